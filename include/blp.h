@@ -1,0 +1,117 @@
+/*
+ * blp.h -- C ABI of the B200 batched two-phase dense simplex (libblp.so).
+ *
+ * The reference (batchlp 0.1.0, /root/reference/pkg/src/batchlp) is a pure
+ * Python package with no C ABI.  Its drop-in boundary for the hot path is the
+ * Python pair re-exported from batchlp/__init__.py:3-12,37:
+ *
+ *   batch_solve(lps, config) -> BatchReport      batch.py:134-179
+ *   solve(lp, limits)        -> SolveOutcome     simplex.py:154-194
+ *
+ * Every entry point below replaces the per-LP body of those functions
+ * (validate -> build_tableau -> phase 1 -> restore_objective -> phase 2 ->
+ * _extract_point) for a whole packed batch; the Python package
+ * paper_1802_08557_b200 keeps the reference's object API on top of it
+ * (INTEGRATION.md shows the ctypes binding).  Plain pointers and sizes only.
+ *
+ * Input layout (packed, same shape (m, n) for the whole batch, as
+ * batch.py:141-144 requires):
+ *   A  [count][m][n] fp64 row-major   (StandardFormLP.A, model.py:105-107)
+ *   b  [count][m]    fp64
+ *   c  [count][n]    fp64
+ * With shared_Ab != 0 (support-function mode) A is [m][n] and b is [m],
+ * shared by every LP; only c differs per LP.
+ *
+ * Output layout:
+ *   status     [count] int8   BLP_STATUS_* (model.py:29-33 order)
+ *   objective  [count] fp64   c.x when OPTIMAL, NaN otherwise (simplex.py:187-194)
+ *   x          [count][n] fp64 primal point when OPTIMAL, zeros otherwise
+ *   iters1/2   [count] int32  pivots in phase 1 / phase 2 (SolveOutcome, model.py:137-138)
+ *
+ * Results are bit-identical to the reference's pivot sequence: status, x and
+ * iteration counts equal the reference's exactly; objective agrees to 1e-9
+ * relative (the reference sums c.x with BLAS ddot, whose order is unpinned).
+ * Validation (non-finite inputs, model.py:263-301) is the caller's job.
+ */
+#ifndef BLP_H_
+#define BLP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLP_ABI_VERSION 1
+
+/* Per-LP status codes.  0-3 mirror Status (model.py:29-33). */
+#define BLP_STATUS_OPTIMAL 0
+#define BLP_STATUS_UNBOUNDED 1
+#define BLP_STATUS_INFEASIBLE 2
+#define BLP_STATUS_ITERATION_LIMIT 3
+/* phase 1 reported unbounded: the reference raises RuntimeError (simplex.py:173-175) */
+#define BLP_STATUS_ERR_PHASE1_UNBOUNDED 4
+
+/* Return codes of the entry points. */
+#define BLP_OK 0
+#define BLP_ERR_INVALID -1     /* bad argument (negative sizes, null pointers) */
+#define BLP_ERR_CUDA -2        /* CUDA runtime error; see blp_last_error() */
+#define BLP_ERR_TOO_LARGE -3   /* the LP shape exceeds every kernel variant */
+
+/* SolverLimits, simplex.py:34-60.  Tolerances are the reference's module
+ * constants (tableau.py:37-39, simplex.py:26-31) compiled into the kernels. */
+typedef struct blp_limits {
+    int32_t max_iterations;   /* <= 0: 50*(m+n) per phase (SolverLimits.iterations_for) */
+    int32_t anti_cycling;     /* 0 or 1 (SolverLimits.anti_cycling)                    */
+    int32_t degenerate_limit; /* < 0: max(m,1) (SolverLimits.bland_trigger)             */
+    int32_t reserved;         /* must be 0                                              */
+} blp_limits;
+
+/*
+ * Device-resident batch solve.  All array pointers are device pointers on
+ * `device`'s current context; work is enqueued on `cuda_stream` (a
+ * cudaStream_t, NULL = legacy default stream) and the call returns without
+ * synchronising.  Replaces the per-LP loop of batch.py:162-173 / simplex.py:154-194.
+ */
+int blp_solve_batch_device(const double *A, const double *b, const double *c,
+                           int64_t count, int32_t m, int32_t n, int32_t shared_Ab,
+                           const blp_limits *limits,
+                           int8_t *status, double *objective, double *x,
+                           int32_t *iters1, int32_t *iters2,
+                           void *cuda_stream);
+
+/*
+ * Host-buffer batch solve (the reference-facing call: batch_solve's
+ * Sequence[StandardFormLP] packed into host arrays).  Copies inputs to
+ * `device`, solves, copies results back, and returns when the host output
+ * buffers are filled.  Large batches are pipelined in sub-batches over
+ * several streams so host<->device copies overlap the kernels.  Pinned host
+ * buffers give full PCIe bandwidth; pageable ones work but copy slower.
+ */
+int blp_solve_batch_host(const double *A, const double *b, const double *c,
+                         int64_t count, int32_t m, int32_t n, int32_t shared_Ab,
+                         const blp_limits *limits,
+                         int8_t *status, double *objective, double *x,
+                         int32_t *iters1, int32_t *iters2,
+                         int32_t device);
+
+/* Largest (m, n) the library accepts: 1 if supported, 0 otherwise. */
+int blp_shape_supported(int32_t m, int32_t n);
+
+/* Name of the kernel variant blp_solve_* would use for (m, n) (static string). */
+const char *blp_kernel_variant(int32_t m, int32_t n);
+
+/* Number of CUDA kernels this library has launched since load (monotonic). */
+int64_t blp_launch_count(void);
+
+/* Text of the last error on the calling thread ("" if none). */
+const char *blp_last_error(void);
+
+/* BLP_ABI_VERSION of the loaded library. */
+int blp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLP_H_ */

@@ -1,0 +1,139 @@
+"""ctypes binding of libblp.so (include/blp.h).
+
+The CUDA library is the product: there is no CPU fallback.  If the shared
+object is missing, or no CUDA device is visible, every solve raises
+``NativeUnavailable`` instead of silently computing on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("BLP_LIBRARY", PKG_DIR / "libblp.so"))
+
+BLP_OK = 0
+ERRORS = {-1: "invalid arguments", -2: "CUDA error", -3: "LP shape too large"}
+
+
+class NativeUnavailable(RuntimeError):
+    """libblp.so cannot be loaded or no CUDA device is usable."""
+
+
+class NativeError(RuntimeError):
+    """libblp.so returned an error code."""
+
+
+class Limits(ctypes.Structure):
+    """blp_limits (include/blp.h) = SolverLimits (simplex.py:34-60)."""
+
+    _fields_ = [("max_iterations", ctypes.c_int32),
+                ("anti_cycling", ctypes.c_int32),
+                ("degenerate_limit", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+
+# Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
+EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
+           "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version")
+
+
+def load():
+    """Load libblp.so (no CUDA call is made here)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeUnavailable(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    P = ctypes.c_void_p
+    sig = [P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+           ctypes.POINTER(Limits), P, P, P, P, P]
+    lib.blp_solve_batch_device.argtypes = sig + [P]
+    lib.blp_solve_batch_device.restype = ctypes.c_int
+    lib.blp_solve_batch_host.argtypes = sig + [ctypes.c_int32]
+    lib.blp_solve_batch_host.restype = ctypes.c_int
+    lib.blp_shape_supported.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.blp_shape_supported.restype = ctypes.c_int
+    lib.blp_kernel_variant.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.blp_kernel_variant.restype = ctypes.c_char_p
+    lib.blp_launch_count.argtypes = []
+    lib.blp_launch_count.restype = ctypes.c_int64
+    lib.blp_last_error.argtypes = []
+    lib.blp_last_error.restype = ctypes.c_char_p
+    lib.blp_abi_version.argtypes = []
+    lib.blp_abi_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != BLP_OK:
+        msg = load().blp_last_error().decode(errors="replace")
+        raise NativeError(f"libblp: {ERRORS.get(rc, rc)}: {msg}")
+
+
+def _require_gpu() -> None:
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device is visible; the batched simplex runs only on the GPU")
+
+
+def make_limits(max_iterations=None, anti_cycling=True, degenerate_pivot_limit=None) -> Limits:
+    return Limits(0 if max_iterations is None else int(max_iterations),
+                  1 if anti_cycling else 0,
+                  -1 if degenerate_pivot_limit is None else int(degenerate_pivot_limit), 0)
+
+
+def kernel_variant(m: int, n: int) -> str:
+    return load().blp_kernel_variant(m, n).decode()
+
+
+def launch_count() -> int:
+    return int(load().blp_launch_count())
+
+
+def solve_host(A: np.ndarray, b: np.ndarray, c: np.ndarray, limits: Limits, *, shared_Ab: bool = False,
+               device: int = 0, out: dict | None = None) -> dict:
+    """Host arrays in, host arrays out (blp_solve_batch_host).  A/b/c must be C-contiguous fp64."""
+    lib = load()
+    _require_gpu()
+    count, n = c.shape
+    m = b.shape[-1]
+    if out is None:
+        out = dict(status=np.empty(count, np.int8), objective=np.empty(count, np.float64),
+                   x=np.empty((count, n), np.float64), it1=np.empty(count, np.int32),
+                   it2=np.empty(count, np.int32))
+    _check(lib.blp_solve_batch_host(_ptr(A), _ptr(b), _ptr(c), count, m, n, 1 if shared_Ab else 0,
+                                    ctypes.byref(limits), _ptr(out["status"]), _ptr(out["objective"]),
+                                    _ptr(out["x"]), _ptr(out["it1"]), _ptr(out["it2"]), int(device)))
+    return out
+
+
+def solve_device(A, b, c, limits: Limits, out: dict, *, shared_Ab: bool = False, stream=None) -> None:
+    """torch CUDA tensors in/out (blp_solve_batch_device); enqueued on `stream`, not synchronised."""
+    import torch
+    lib = load()
+    count, n = c.shape
+    m = b.shape[-1]
+    if stream is None:
+        stream = torch.cuda.current_stream(c.device)
+    _check(lib.blp_solve_batch_device(A.data_ptr(), b.data_ptr(), c.data_ptr(), count, m, n,
+                                      1 if shared_Ab else 0, ctypes.byref(limits),
+                                      out["status"].data_ptr(), out["objective"].data_ptr(),
+                                      out["x"].data_ptr(), out["it1"].data_ptr(), out["it2"].data_ptr(),
+                                      ctypes.c_void_p(stream.cuda_stream)))
+
+
+def _ptr(a) -> int:
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    return a.data_ptr()  # torch tensor (pinned host or device)

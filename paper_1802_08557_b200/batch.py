@@ -1,0 +1,308 @@
+"""Batched entry points of the drop-in.
+
+``batch_solve(lps, config) -> BatchReport`` keeps the reference signature and
+result layout (/root/reference/pkg/src/batchlp/batch.py:134-179): same-shape
+check (``HeterogeneousBatch``, :141-144), the Algorithm-1 chunk plan computed
+with the batch-worst artificial count (:146-153, ``lp_memory_bytes`` :98-106,
+``plan_chunks`` :109-127, ``BatchTooLarge``), outcomes in input order, one
+``chunk_seconds`` entry per planned chunk, ``total_seconds``.
+
+What changes is underneath: the LPs are packed once into contiguous arrays
+(one ``np.asarray``), validated with one vectorised ``np.isfinite`` pass, and
+each planned chunk is one call into libblp.so, which pipelines sub-batches
+over CUDA streams on the GPU(s).  ``worker_count`` stays what it is in the
+reference -- a throughput knob that never changes results -- and is unused
+by the GPU path; ``devices`` chooses the GPUs (contiguous LP-index shards,
+no collective).
+
+``batch_solve_arrays`` / ``support_batch`` are the packed fast paths that
+skip the ``StandardFormLP`` / ``SolveOutcome`` object layers.
+"""
+from __future__ import annotations
+
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .model import SolveOutcome, StandardFormLP, STATUS_BY_CODE, first_nonfinite, invalid_message, validate
+from .simplex import PHASE1_UNBOUNDED_MESSAGE, SolverLimits, outcome_from_arrays
+
+# Column ceiling of the paper's one-block-per-LP Kepler kernel (batch.py:25-29);
+# informational, as in the reference.  The B200 kernels have no such limit.
+REFERENCE_GPU_BLOCK_COLS = 1024
+
+
+class BatchTooLarge(Exception):
+    """A single LP's tableau exceeds the memory budget."""
+
+
+class HeterogeneousBatch(Exception):
+    """The LPs in a batch do not all share one (m, n) shape."""
+
+
+@dataclass(frozen=True)
+class BatchConfig:
+    """Knobs for one batched run (batch.py:40-58) plus the GPU selection.
+
+    ``memory_budget_bytes`` governs the chunk plan only; ``worker_count`` is
+    accepted for compatibility (results never depend on it); ``devices``
+    lists the CUDA devices the batch is sharded over (default: device 0).
+    """
+
+    memory_budget_bytes: int = 1 << 30
+    worker_count: int = 1
+    limits: SolverLimits = field(default_factory=SolverLimits)
+    data_size_bytes: int = 8
+    devices: tuple[int, ...] = (0,)
+
+    def __post_init__(self):
+        if self.memory_budget_bytes <= 0:
+            raise ValueError("memory_budget_bytes must be positive")
+        if self.worker_count < 1:
+            raise ValueError("worker_count must be >= 1")
+        if len(self.devices) < 1:
+            raise ValueError("devices must name at least one CUDA device")
+
+
+@dataclass(frozen=True)
+class ChunkPlan:
+    """Contiguous [start, end) pieces covering the batch, in order (batch.py:61-74)."""
+
+    batch_size: int
+    bounds: tuple[tuple[int, int], ...]
+
+    @property
+    def sizes(self) -> tuple[int, ...]:
+        return tuple(e - s for s, e in self.bounds)
+
+    @property
+    def count(self) -> int:
+        return len(self.bounds)
+
+
+@dataclass
+class BatchReport:
+    """Outcomes in input order plus plan and timings (batch.py:77-95)."""
+
+    outcomes: list[SolveOutcome]
+    plan: ChunkPlan
+    chunk_seconds: list[float]
+    total_seconds: float
+
+    @property
+    def lps_per_second(self) -> float:
+        if self.total_seconds <= 0:
+            return float("inf")
+        return len(self.outcomes) / self.total_seconds
+
+    def status_counts(self) -> dict[str, int]:
+        counts: dict[str, int] = {}
+        for o in self.outcomes:
+            counts[o.status.value] = counts.get(o.status.value, 0) + 1
+        return counts
+
+
+def lp_memory_bytes(m: int, n: int, num_slack: int, num_artificial: int, data_size_bytes: int = 8) -> int:
+    """Reference per-LP footprint (Eq. 5): tableau + two scan arrays (batch.py:98-106)."""
+    cols = n + num_slack + num_artificial + 2
+    return (m + 1 + 2) * cols * data_size_bytes
+
+
+def plan_chunks(count: int, lp_bytes: int, config: BatchConfig) -> ChunkPlan:
+    """Algorithm 1 (batch.py:109-127): chunks of floor(S / lp_bytes) LPs, last one the remainder."""
+    if lp_bytes > config.memory_budget_bytes:
+        raise BatchTooLarge(f"one LP needs {lp_bytes} bytes but the budget is {config.memory_budget_bytes}")
+    if count == 0:
+        return ChunkPlan(batch_size=0, bounds=())
+    size = config.memory_budget_bytes // lp_bytes
+    if count <= size:
+        return ChunkPlan(batch_size=size, bounds=((0, count),))
+    return ChunkPlan(batch_size=size, bounds=tuple(
+        (k * size, min((k + 1) * size, count)) for k in range(math.ceil(count / size))))
+
+
+# ---------------------------------------------------------------------------
+# packed fast paths
+
+@dataclass
+class BatchArrays:
+    """Packed results: status codes (include/blp.h), objective (NaN unless optimal),
+    x [B, n] (zeros unless optimal), per-phase iteration counts."""
+
+    status: np.ndarray
+    objective: np.ndarray
+    x: np.ndarray
+    iterations_phase1: np.ndarray
+    iterations_phase2: np.ndarray
+
+    def outcome(self, k: int) -> SolveOutcome:
+        return outcome_from_arrays(self._as_dict(), k)
+
+    def outcomes(self) -> list[SolveOutcome]:
+        d = self._as_dict()
+        return [outcome_from_arrays(d, k) for k in range(len(self.status))]
+
+    def status_counts(self) -> dict[str, int]:
+        codes, counts = np.unique(self.status, return_counts=True)
+        return {STATUS_BY_CODE[c].value: int(k) for c, k in zip(codes, counts) if c < len(STATUS_BY_CODE)}
+
+    def _as_dict(self) -> dict:
+        return dict(status=self.status, objective=self.objective, x=self.x,
+                    it1=self.iterations_phase1, it2=self.iterations_phase2)
+
+
+def _as_f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared_Ab: bool,
+                   out: dict | None = None) -> dict:
+    """Contiguous LP-index shards, one host thread per device (ctypes releases the GIL)."""
+    count, n = c.shape
+    if out is None:
+        out = dict(status=np.empty(count, np.int8), objective=np.empty(count, np.float64),
+                   x=np.empty((count, n), np.float64), it1=np.empty(count, np.int32),
+                   it2=np.empty(count, np.int32))
+    lim = limits.to_native()
+    devices = list(devices)[:max(1, count)]
+    if len(devices) == 1 or count == 0:
+        if count:
+            _native.solve_host(A, b, c, lim, shared_Ab=shared_Ab, device=devices[0], out=out)
+        return out
+    per = -(-count // len(devices))
+    errors: list[BaseException] = []
+
+    def work(dev: int, s: int, e: int) -> None:
+        try:
+            sub = {k: v[s:e] for k, v in out.items()}
+            _native.solve_host(A if shared_Ab else A[s:e], b if shared_Ab else b[s:e], c[s:e], lim,
+                               shared_Ab=shared_Ab, device=dev, out=sub)
+        except BaseException as err:  # re-raised on the caller's thread
+            errors.append(err)
+
+    threads = [threading.Thread(target=work, args=(d, k * per, min(count, (k + 1) * per)))
+               for k, d in enumerate(devices) if k * per < count]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out
+
+
+def batch_solve_arrays(A, b, c, limits: SolverLimits = SolverLimits(), *, devices: Sequence[int] = (0,),
+                       check_finite: bool = True) -> BatchArrays:
+    """Solve a packed batch: A [B,m,n], b [B,m], c [B,n] (fp64).  GPU only.
+
+    Raises ValueError (reference message) for the first LP with a non-finite
+    entry and RuntimeError if any LP's phase 1 reports unbounded.
+    """
+    A, b, c = _as_f64(A), _as_f64(b), _as_f64(c)
+    if A.ndim != 3 or b.ndim != 2 or c.ndim != 2 or A.shape != (c.shape[0], b.shape[1], c.shape[1]) \
+            or b.shape[0] != c.shape[0]:
+        raise ValueError(f"packed shapes disagree: A {A.shape}, b {b.shape}, c {c.shape}")
+    if check_finite:
+        k = first_nonfinite(A, b, c)
+        if k >= 0:
+            raise ValueError(invalid_message(validate(StandardFormLP(c=c[k], A=A[k], b=b[k]))))
+    res = _solve_sharded(A, b, c, limits, devices, shared_Ab=False)
+    return _finish(res)
+
+
+def support_batch(A, b, C, limits: SolverLimits = SolverLimits(), *, devices: Sequence[int] = (0,)) -> BatchArrays:
+    """Support-function mode: one polytope A x <= b (A [m,n], b [m]) and many
+    objective directions C [B,n]; LP k maximises C[k].x over the polytope.
+
+    Same results as batch_solve over [StandardFormLP(C[k], A, b)],
+    without replicating A per LP.
+    """
+    A, b, C = _as_f64(A), _as_f64(b), _as_f64(C)
+    if A.ndim != 2 or b.ndim != 1 or C.ndim != 2 or A.shape != (b.shape[0], C.shape[1]):
+        raise ValueError(f"support shapes disagree: A {A.shape}, b {b.shape}, C {C.shape}")
+    if not (np.isfinite(A).all() and np.isfinite(b).all()) and len(C):
+        raise ValueError(invalid_message(validate(StandardFormLP(c=C[0], A=A, b=b))))
+    bad = np.flatnonzero(~np.isfinite(C).all(axis=1))
+    if bad.size:
+        raise ValueError(invalid_message(validate(StandardFormLP(c=C[bad[0]], A=A, b=b))))
+    res = _solve_sharded(A, b, C, limits, devices, shared_Ab=True)
+    return _finish(res)
+
+
+def _finish(res: dict) -> BatchArrays:
+    if (res["status"] == 4).any():
+        raise RuntimeError(PHASE1_UNBOUNDED_MESSAGE)
+    return BatchArrays(res["status"], res["objective"], res["x"], res["it1"], res["it2"])
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible object API
+
+def _first_bad_shape(lps: list, m: int, n: int) -> int:
+    """Lowest index whose A is not (m, n), or -1."""
+    for k, lp in enumerate(lps):
+        try:
+            ok = np.shape(lp.A) == (m, n)
+        except ValueError:  # ragged rows
+            ok = False
+        if not ok:
+            return k
+    return -1
+
+
+def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig()) -> BatchReport:
+    """Solve every LP of a same-shaped batch on the GPU; outcomes land at their input index."""
+    lps = list(lps)
+    shapes = {(lp.m, lp.n) for lp in lps}
+    if len(shapes) > 1:
+        raise HeterogeneousBatch(f"batch mixes LP shapes {sorted(shapes)}")
+    if lps:
+        m, n = next(iter(shapes))
+        worst_artificial = max(int(np.sum(np.asarray(lp.b) < 0)) for lp in lps)
+        lp_bytes = lp_memory_bytes(m, n, num_slack=m, num_artificial=worst_artificial,
+                                   data_size_bytes=config.data_size_bytes)
+    else:
+        lp_bytes = 1
+    plan = plan_chunks(len(lps), lp_bytes, config)
+    if not lps:
+        return BatchReport(outcomes=[], plan=plan, chunk_seconds=[], total_seconds=0.0)
+
+    # Pack once, validate once.  The reference raises at the first invalid LP
+    # in index order (solve() inside the chunk loop), after solving the ones
+    # before it; a phase-1-unbounded LP earlier in the batch raises first.
+    bad_shape = _first_bad_shape(lps, m, n)
+    limit = bad_shape if bad_shape >= 0 else len(lps)
+    A = np.empty((limit, m, n), np.float64)
+    b = np.empty((limit, m), np.float64)
+    c = np.empty((limit, n), np.float64)
+    for k in range(limit):
+        lp = lps[k]
+        A[k] = lp.A
+        b[k] = lp.b
+        c[k] = lp.c
+    bad_value = first_nonfinite(A, b, c)
+    first_bad = bad_value if bad_value >= 0 else bad_shape
+    if first_bad >= 0:
+        if first_bad:
+            res = _solve_sharded(A[:first_bad], b[:first_bad], c[:first_bad], config.limits,
+                                 config.devices, shared_Ab=False)
+            if (res["status"] == 4).any():
+                raise RuntimeError(PHASE1_UNBOUNDED_MESSAGE)
+        raise ValueError(invalid_message(validate(lps[first_bad])))
+
+    outcomes: list[SolveOutcome | None] = [None] * len(lps)
+    chunk_seconds: list[float] = []
+    started = time.perf_counter()
+    for start, end in plan.bounds:
+        t0 = time.perf_counter()
+        res = _solve_sharded(A[start:end], b[start:end], c[start:end], config.limits,
+                             config.devices, shared_Ab=False)
+        outcomes[start:end] = [outcome_from_arrays(res, k) for k in range(end - start)]
+        chunk_seconds.append(time.perf_counter() - t0)
+    total = time.perf_counter() - started
+    return BatchReport(outcomes=outcomes, plan=plan, chunk_seconds=chunk_seconds, total_seconds=total)

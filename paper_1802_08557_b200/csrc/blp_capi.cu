@@ -1,0 +1,297 @@
+// blp_capi.cu -- C ABI of libblp.so (declared in include/blp.h).
+//
+// Host runtime around the simplex kernels: variant selection by LP shape,
+// persistent-grid sizing from the occupancy calculator, stream-ordered
+// workspace, and the host-buffer path that pipelines sub-batches over
+// several streams so H2D / kernel / D2H overlap (the paper's multi-stream
+// scheme, on B200's independent copy engines).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/blp.h"
+#include "blp_common.cuh"
+#include "blp_tableau_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define BLP_CUDA_TRY(expr)                                                              \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(BLP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+constexpr size_t kMaxDynSmem = 227 * 1024;
+
+using KernelFn = void (*)(blp::Batch);
+
+struct Variant {
+    KernelFn fn;
+    const char *name;
+    bool smem_tab;
+    int max_threads;
+};
+
+// Rows per lane (RPL) = ceil((m+1)/32) selects the register footprint.
+Variant pick_variant(int m, int n, bool *ok) {
+    const int rows = m + 1;
+    const int rpl = (rows + 31) / 32;
+    const blp::TabLayout Ls = blp::make_tab_layout(m, n, 32, true);
+    *ok = true;
+    if (Ls.bytes <= kMaxDynSmem) {
+        switch (rpl) {
+            case 1: return {blp::tableau_kernel<1, true, 1024>, "smem_rpl1", true, 1024};
+            case 2: return {blp::tableau_kernel<2, true, 1024>, "smem_rpl2", true, 1024};
+            case 3: return {blp::tableau_kernel<3, true, 1024>, "smem_rpl3", true, 1024};
+            case 4: return {blp::tableau_kernel<4, true, 1024>, "smem_rpl4", true, 1024};
+            default: break;
+        }
+    }
+    if (rpl <= 1) return {blp::tableau_kernel<1, false, 1024>, "hbm_rpl1", false, 1024};
+    if (rpl <= 2) return {blp::tableau_kernel<2, false, 1024>, "hbm_rpl2", false, 1024};
+    if (rpl <= 4) return {blp::tableau_kernel<4, false, 1024>, "hbm_rpl4", false, 1024};
+    if (rpl <= 8) return {blp::tableau_kernel<8, false, 512>, "hbm_rpl8", false, 512};
+    if (rpl <= 16) return {blp::tableau_kernel<16, false, 512>, "hbm_rpl16", false, 512};
+    if (rpl <= 32) return {blp::tableau_kernel<32, false, 256>, "hbm_rpl32", false, 256};
+    *ok = false;
+    return {nullptr, "unsupported", false, 0};
+}
+
+struct DeviceInfo {
+    int sms = 0;
+    bool init = false;
+};
+std::mutex g_mu;
+DeviceInfo g_dev[64];
+
+int device_sms(int dev, int *sms) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return fail(BLP_ERR_INVALID, "device index out of range");
+    if (!g_dev[dev].init) {
+        BLP_CUDA_TRY(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ~0ull;  // keep freed blocks cached between calls
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        g_dev[dev].init = true;
+    }
+    *sms = g_dev[dev].sms;
+    return BLP_OK;
+}
+
+// Threads per CTA: enough warps that the resident CTAs of one SM hold about
+// 32 warps (register budget ~64/thread), never more warps than columns.
+int pick_threads(const Variant &v, int m, int n, size_t smem) {
+    const int ncols = n + m + 1;
+    int ctas = v.smem_tab ? (int)std::max<size_t>(1, (228 * 1024) / (smem + 1024)) : 2;
+    ctas = std::min(ctas, 16);
+    int warps = std::max(2, 32 / ctas);
+    warps = std::min(warps, std::max(1, (ncols + 1) / 2));
+    warps = std::min(warps, v.max_threads / 32);
+    return std::max(1, warps) * 32;
+}
+
+int launch_solve(const double *A, const double *b, const double *c, long long count, int m, int n,
+                 int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
+                 int32_t *it1, int32_t *it2, cudaStream_t stream) {
+    if (count == 0) return BLP_OK;
+    int dev = 0;
+    BLP_CUDA_TRY(cudaGetDevice(&dev));
+    int sms = 0;
+    int rc = device_sms(dev, &sms);
+    if (rc) return rc;
+    bool ok = false;
+    Variant v = pick_variant(m, n, &ok);
+    if (!ok) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
+    // threads first (layout size depends only weakly on it), then smem
+    blp::TabLayout L = blp::make_tab_layout(m, n, 32, v.smem_tab);
+    const int threads = pick_threads(v, m, n, L.bytes);
+    L = blp::make_tab_layout(m, n, threads / 32, v.smem_tab);
+    BLP_CUDA_TRY(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+    int occ = 0;
+    BLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, threads, L.bytes));
+    if (occ < 1) return fail(BLP_ERR_TOO_LARGE, "kernel variant cannot be resident on an SM");
+    long long grid = (long long)occ * sms;
+    if (grid > count) grid = count;
+
+    const long long slot = v.smem_tab ? 0 : (long long)L.ncols * L.ld;
+    const size_t ws_bytes = 256 + (size_t)slot * sizeof(double) * (size_t)grid;
+    void *ws = nullptr;
+    BLP_CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, stream));
+    BLP_CUDA_TRY(cudaMemsetAsync(ws, 0, 256, stream));
+
+    blp::Batch B;
+    B.A = A; B.b = b; B.c = c; B.count = count; B.m = m; B.n = n; B.shared_Ab = shared_Ab;
+    B.status = status; B.objective = objective; B.x = x; B.it1 = it1; B.it2 = it2;
+    B.next_lp = reinterpret_cast<int *>(ws);
+    B.gtab = v.smem_tab ? nullptr : reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
+    B.gtab_stride = slot;
+    B.lim.max_iterations = lim ? lim->max_iterations : 0;
+    B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
+    B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
+    B.lim.reserved = 0;
+
+    v.fn<<<(unsigned)grid, threads, L.bytes, stream>>>(B);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    BLP_CUDA_TRY(cudaGetLastError());
+    BLP_CUDA_TRY(cudaFreeAsync(ws, stream));
+    return BLP_OK;
+}
+
+bool bad_args(const double *A, const double *b, const double *c, long long count, int m, int n,
+              const int8_t *status, const double *objective, const double *x, const int32_t *it1,
+              const int32_t *it2) {
+    if (count < 0 || m < 0 || n < 0) return true;
+    if (count == 0) return false;
+    if ((m > 0 && (!b || (n > 0 && !A))) || (n > 0 && (!c || !x))) return true;
+    return !status || !objective || !it1 || !it2;
+}
+
+struct StreamSet {
+    std::vector<cudaStream_t> s;
+};
+StreamSet g_streams[64];
+
+}  // namespace
+
+extern "C" {
+
+int blp_abi_version(void) { return BLP_ABI_VERSION; }
+
+const char *blp_last_error(void) { return g_last_error.c_str(); }
+
+int64_t blp_launch_count(void) { return g_launches.load(); }
+
+int blp_shape_supported(int32_t m, int32_t n) {
+    bool ok = false;
+    if (m < 0 || n < 0) return 0;
+    pick_variant(m, n, &ok);
+    return ok ? 1 : 0;
+}
+
+const char *blp_kernel_variant(int32_t m, int32_t n) {
+    bool ok = false;
+    if (m < 0 || n < 0) return "invalid";
+    return pick_variant(m, n, &ok).name;
+}
+
+int blp_solve_batch_device(const double *A, const double *b, const double *c, int64_t count,
+                           int32_t m, int32_t n, int32_t shared_Ab, const blp_limits *limits,
+                           int8_t *status, double *objective, double *x, int32_t *iters1,
+                           int32_t *iters2, void *cuda_stream) {
+    g_last_error.clear();
+    if (bad_args(A, b, c, count, m, n, status, objective, x, iters1, iters2))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    return launch_solve(A, b, c, count, m, n, shared_Ab, limits, status, objective, x, iters1, iters2,
+                        reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+int blp_solve_batch_host(const double *A, const double *b, const double *c, int64_t count,
+                         int32_t m, int32_t n, int32_t shared_Ab, const blp_limits *limits,
+                         int8_t *status, double *objective, double *x, int32_t *iters1,
+                         int32_t *iters2, int32_t device) {
+    g_last_error.clear();
+    if (bad_args(A, b, c, count, m, n, status, objective, x, iters1, iters2))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    if (device < 0 || device >= 64) return fail(BLP_ERR_INVALID, "device index out of range");
+    BLP_CUDA_TRY(cudaSetDevice(device));
+    constexpr int kStreams = 3;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto &ss = g_streams[device].s;
+        if (ss.empty()) {
+            ss.resize(kStreams);
+            for (auto &s : ss) BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        }
+    }
+    const auto &ss = g_streams[device].s;
+    // Sub-batches: at least 8192 LPs each, at most 8 of them.
+    const long long chunk = std::max<long long>(8192, (count + 7) / 8);
+    const size_t szA = (size_t)m * n, szb = (size_t)m;
+
+    // Shared polytope (support-function mode): one H2D, every stream waits on it.
+    double *dA_shared = nullptr, *db_shared = nullptr;
+    cudaEvent_t shared_ready = nullptr;
+    if (shared_Ab) {
+        BLP_CUDA_TRY(cudaMallocAsync(&dA_shared, std::max<size_t>(1, szA) * sizeof(double), ss[0]));
+        BLP_CUDA_TRY(cudaMallocAsync(&db_shared, std::max<size_t>(1, szb) * sizeof(double), ss[0]));
+        if (szA) BLP_CUDA_TRY(cudaMemcpyAsync(dA_shared, A, szA * sizeof(double), cudaMemcpyHostToDevice, ss[0]));
+        if (szb) BLP_CUDA_TRY(cudaMemcpyAsync(db_shared, b, szb * sizeof(double), cudaMemcpyHostToDevice, ss[0]));
+        BLP_CUDA_TRY(cudaEventCreateWithFlags(&shared_ready, cudaEventDisableTiming));
+        BLP_CUDA_TRY(cudaEventRecord(shared_ready, ss[0]));
+        for (int k = 1; k < kStreams; ++k) BLP_CUDA_TRY(cudaStreamWaitEvent(ss[k], shared_ready, 0));
+    }
+    int rc = BLP_OK;
+    int ci = 0;
+    for (long long start = 0; start < count && rc == BLP_OK; start += chunk, ++ci) {
+        const long long cnt = std::min(chunk, count - start);
+        cudaStream_t s = ss[ci % kStreams];
+        const size_t bytes_in = shared_Ab ? (size_t)cnt * n * 8 : (size_t)cnt * (szA + szb + n) * 8;
+        const size_t bytes_out = (size_t)cnt * (n * 8 + 8 + 1 + 8) + 64;
+        char *buf = nullptr;
+        BLP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes_in + bytes_out + 256, s));
+        double *dA = dA_shared, *db = db_shared, *dc;
+        char *p = buf;
+        if (!shared_Ab) {
+            dA = reinterpret_cast<double *>(p); p += (size_t)cnt * szA * 8;
+            db = reinterpret_cast<double *>(p); p += (size_t)cnt * szb * 8;
+        }
+        dc = reinterpret_cast<double *>(p); p += (size_t)cnt * n * 8;
+        double *dobj = reinterpret_cast<double *>(p); p += (size_t)cnt * 8;
+        double *dx = reinterpret_cast<double *>(p); p += (size_t)cnt * n * 8;
+        int32_t *dit1 = reinterpret_cast<int32_t *>(p); p += (size_t)cnt * 4;
+        int32_t *dit2 = reinterpret_cast<int32_t *>(p); p += (size_t)cnt * 4;
+        int8_t *dst = reinterpret_cast<int8_t *>(p);
+        if (!shared_Ab) {
+            if (szA) BLP_CUDA_TRY(cudaMemcpyAsync(dA, A + start * szA, cnt * szA * 8, cudaMemcpyHostToDevice, s));
+            if (szb) BLP_CUDA_TRY(cudaMemcpyAsync(db, b + start * szb, cnt * szb * 8, cudaMemcpyHostToDevice, s));
+        }
+        if (n) BLP_CUDA_TRY(cudaMemcpyAsync(dc, c + start * n, (size_t)cnt * n * 8, cudaMemcpyHostToDevice, s));
+        rc = launch_solve(dA, db, dc, cnt, m, n, shared_Ab, limits, dst, dobj, dx, dit1, dit2, s);
+        if (rc != BLP_OK) break;
+        BLP_CUDA_TRY(cudaMemcpyAsync(status + start, dst, cnt, cudaMemcpyDeviceToHost, s));
+        BLP_CUDA_TRY(cudaMemcpyAsync(objective + start, dobj, cnt * 8, cudaMemcpyDeviceToHost, s));
+        if (n) BLP_CUDA_TRY(cudaMemcpyAsync(x + start * n, dx, (size_t)cnt * n * 8, cudaMemcpyDeviceToHost, s));
+        BLP_CUDA_TRY(cudaMemcpyAsync(iters1 + start, dit1, cnt * 4, cudaMemcpyDeviceToHost, s));
+        BLP_CUDA_TRY(cudaMemcpyAsync(iters2 + start, dit2, cnt * 4, cudaMemcpyDeviceToHost, s));
+        BLP_CUDA_TRY(cudaFreeAsync(buf, s));
+    }
+    if (shared_Ab) {
+        // the last user of the shared polytope may be any stream
+        for (int k = 1; k < kStreams; ++k) {
+            cudaEvent_t ev;
+            BLP_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            BLP_CUDA_TRY(cudaEventRecord(ev, ss[k]));
+            BLP_CUDA_TRY(cudaStreamWaitEvent(ss[0], ev, 0));
+            BLP_CUDA_TRY(cudaEventDestroy(ev));
+        }
+        BLP_CUDA_TRY(cudaFreeAsync(dA_shared, ss[0]));
+        BLP_CUDA_TRY(cudaFreeAsync(db_shared, ss[0]));
+    }
+    for (int k = 0; k < kStreams; ++k) {
+        cudaError_t e = cudaStreamSynchronize(ss[k]);
+        if (e != cudaSuccess && rc == BLP_OK)
+            rc = fail(BLP_ERR_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(e));
+    }
+    if (shared_ready) cudaEventDestroy(shared_ready);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// blp_common.cuh -- constants, batch descriptor and numpy-exact reductions
+// shared by every simplex kernel variant.
+//
+// Bit-parity rules with the reference (numpy, /root/reference/pkg/src/batchlp):
+//  * every product and sum is rounded separately: __dmul_rn / __dsub_rn /
+//    __dadd_rn (numpy never fuses; nvcc would contract a - f*r into DFMA),
+//    and the library is also compiled with -fmad=false;
+//  * divisions are IEEE round-to-nearest (__ddiv_rn), as numpy's true_divide;
+//  * arg-reductions return the FIRST extreme index, with NaN as the extreme
+//    value, exactly like np.argmax / np.argmin (tableau.py:183, :212,
+//    simplex.py:124).
+#pragma once
+
+#include <climits>
+#include <cstdint>
+
+namespace blp {
+
+// Reference tolerances (tableau.py:37-39, simplex.py:26-31).
+constexpr double kSentinel = 1e308;       // SENTINEL
+constexpr double kTol = 1e-9;             // DEFAULT_TOL
+constexpr double kPhase1ZeroTol = 1e-7;   // PHASE1_ZERO_TOL
+constexpr double kDegenerateTol = 1e-9;   // DEGENERATE_RATIO_TOL
+constexpr double kRedundantTol = 1e-7;    // REDUNDANT_ROW_TOL
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNone = INT_MAX;            // "no candidate" index
+
+// Per-LP status codes, equal to BLP_STATUS_* in include/blp.h.
+enum : int8_t {
+    kOptimal = 0,
+    kUnbounded = 1,
+    kInfeasible = 2,
+    kIterationLimit = 3,
+    kErrPhase1Unbounded = 4,
+};
+
+// SolverLimits (simplex.py:34-60); same layout as blp_limits.
+struct Limits {
+    int max_iterations;    // <= 0: 50*(m+n)
+    int anti_cycling;
+    int degenerate_limit;  // < 0: max(m,1)
+    int reserved;
+};
+
+// One launch's worth of work: a packed batch of same-shaped LPs.
+struct Batch {
+    const double *A;       // [count][m][n] row-major, or [m][n] if shared_Ab
+    const double *b;       // [count][m], or [m] if shared_Ab
+    const double *c;       // [count][n]
+    long long count;
+    int m, n;
+    int shared_Ab;
+    int8_t *status;        // [count]
+    double *objective;     // [count]
+    double *x;             // [count][n]
+    int *it1, *it2;        // [count]
+    int *next_lp;          // LP queue head of the persistent grid, zero at launch
+    double *gtab;          // global tableau slots (HBM-streamed variant), one per CTA
+    long long gtab_stride; // doubles per slot
+    Limits lim;
+};
+
+// np.argmax order: NaN first (lowest index among NaNs), then larger value,
+// then lower index.  kNone marks an empty slot.
+__device__ __forceinline__ bool argmax_before(double a, int ia, double b, int ib) {
+    const bool na = a != a, nb = b != b;
+    if (na || nb) return na && (!nb || ia < ib);
+    return a > b || (a == b && ia < ib);
+}
+
+// np.argmin order: NaN first, then smaller value, then lower index.
+__device__ __forceinline__ bool argmin_before(double a, int ia, double b, int ib) {
+    const bool na = a != a, nb = b != b;
+    if (na || nb) return na && (!nb || ia < ib);
+    return a < b || (a == b && ia < ib);
+}
+
+// Butterfly reductions: every lane ends with the warp-wide winner.
+__device__ __forceinline__ void warp_argmax(double &v, int &i) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, v, off);
+        const int oi = __shfl_xor_sync(kFull, i, off);
+        if (argmax_before(ov, oi, v, i)) { v = ov; i = oi; }
+    }
+}
+
+__device__ __forceinline__ void warp_argmin(double &v, int &i) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, v, off);
+        const int oi = __shfl_xor_sync(kFull, i, off);
+        if (argmin_before(ov, oi, v, i)) { v = ov; i = oi; }
+    }
+}
+
+__device__ __forceinline__ int warp_min_int(int v) {
+    return (int)__reduce_min_sync(kFull, (unsigned)v);
+}
+
+}  // namespace blp
