@@ -1,0 +1,371 @@
+"""Benchmark of the batched two-phase simplex (BASELINE.json metric: LPs solved/sec, fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one batched solve of the whole per-GPU batch.  The default workload
+is BASELINE.json configs[1] (C2): 1e5 afiro-shaped 28x32 LPs with mixed-sign
+b (two-phase), per GPU (weak scaling: every rank solves its own 1e5 LPs,
+contiguous LP-index shards of an N x 1e5 global batch, no collective on the
+data path).  Rank 0 prints one JSON line:
+
+  value      LPs/s over all ranks, inputs resident in HBM (blp_solve_batch_device),
+             CUDA events on the launching stream, max over ranks
+  e2e        same metric through the public API (batch_solve_arrays) from pinned
+             host buffers: H2D of A, b, c + kernels + D2H of every result per step
+  roofline   algorithmic tableau bytes 16(m+1)(n+m+1) per pivot x pivots / kernel
+             time, against the measured smem bandwidth (tableau resident in
+             shared memory) or the measured HBM copy bandwidth (streamed)
+  cpu_baseline  the C oracle port (oracle/, the reference algorithm) on the
+             host cores, rank 0 at N=1, on a bounded sample of the workload
+
+``--impl reference`` times that CPU implementation alone (rank 0; other ranks
+exit 0) on the same config and prints the reference arm's line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LPs solved/sec (batch 1e5, fp64)"
+UNIT = "LPs/s"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--count", type=int, default=None, help="LPs per GPU (default: the config's size)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def workload(cfg: str, count: int | None, rank: int):
+    """Packed inputs of this rank's shard: rank r solves LPs [r*B, (r+1)*B) of the global batch,
+    generated with the config's recipe and seed + 1000*r (rank 0 = the canonical config)."""
+    from paper_1802_08557_b200 import workloads
+    spec = workloads.CONFIGS[cfg]
+    cnt = spec["count"] if count is None else count
+    if cfg == "c1":
+        A, b, c = workloads.random_arrays(5, cnt, 0 + 1000 * rank)
+        shared = False
+    elif cfg == "c2":
+        A, b, c = workloads.afiro_arrays(cnt, seed=2 + 1000 * rank)
+        shared = False
+    elif cfg == "c3":
+        A, b, c = workloads.degenerate_arrays(cnt, seed=3 + 1000 * rank)
+        shared = False
+    elif cfg == "c4":
+        A, b = workloads.support_polytope()
+        c = workloads.support_directions(cnt, offset=rank * cnt)
+        shared = True
+    else:
+        A, b, c = workloads.random_arrays(500, cnt, 5 + 1000 * rank)
+        shared = False
+    return A, b, c, shared, spec
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.2)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+def bytes_per_pivot(m: int, n: int) -> int:
+    """Algorithmic tableau bytes per pivot: one read + one write of (m+1)(n+m+1) fp64 cells."""
+    return 16 * (m + 1) * (n + m + 1)
+
+
+def measured_hbm_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> dict:
+    """The oracle port (reference algorithm in C) on all host cores, bounded sample."""
+    from oracle import oracle
+    cores = oracle.host_cores()
+    probe = min(len(c), 2000)
+    t0 = time.perf_counter()
+    oracle.solve_batch(A if shared else A[:probe], b if shared else b[:probe], c[:probe], shared_Ab=shared,
+                       threads=cores)
+    rate = probe / max(1e-6, time.perf_counter() - t0)
+    sample = int(min(len(c), max(probe, rate * target_s)))
+    t0 = time.perf_counter()
+    res = oracle.solve_batch(A if shared else A[:sample], b if shared else b[:sample], c[:sample],
+                             shared_Ab=shared, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": UNIT, "cores": int(res["threads"]), "kind": "port",
+            "sample": f"first {sample} LPs of this config's rank-0 batch, oracle/blp_oracle.c "
+                      f"(full reference tableau incl. artificial columns), {res['threads']} threads, {dt:.2f} s",
+            "pivots_per_s": float((res["it1"] + res["it2"]).sum() / dt)}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    A, b, c, shared, spec = workload(args.config, args.count, 0)
+    from oracle import oracle
+    cores = oracle.host_cores()
+    # size one step at ~2 s of host work so warmup+steps finish in a few minutes
+    probe = min(len(c), 2000)
+    t0 = time.perf_counter()
+    oracle.solve_batch(A if shared else A[:probe], b if shared else b[:probe], c[:probe], shared_Ab=shared,
+                       threads=cores)
+    rate = probe / max(1e-6, time.perf_counter() - t0)
+    sample = int(min(len(c), max(probe, rate * 2.0)))
+    sl = (lambda v: v) if shared else (lambda v: v[:sample])
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = oracle.solve_batch(sl(A), sl(b), c[:sample], shared_Ab=shared, threads=cores)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step = statistics.median(times)
+    value = sample / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args, spec, len(c), shared),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(res["threads"]), "kind": "port",
+                         "sample": f"first {sample} LPs of the rank-0 batch per step, oracle/blp_oracle.c "
+                                   f"(C restatement of batchlp tableau.py/simplex.py), median of {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pivots_per_s": float((res["it1"] + res["it2"]).sum() / step),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, spec, count, shared) -> dict:
+    from paper_1802_08557_b200 import workloads
+    m, n = spec["m"], spec["n"]
+    return {"workload": f"{args.config}: {spec['doc']}", "m": m, "n": n, "lps_per_gpu": count,
+            "global_batch": count * args.gpus, "support_function": shared,
+            "parallelism": f"lp-index shards x{args.gpus} (no collective)",
+            "l2": "inputs > 126 MB L2 per step (no flush needed)" if count * (m * n + m + n) * 8 > 126e6
+            else "inputs fit L2; L2 flushed between steps"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_1802_08557_b200 import SolverLimits, _native, batch_solve_arrays
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    A, b, c, shared, spec = workload(args.config, args.count, rank)
+    count, n = c.shape
+    m = b.shape[-1]
+    lim = SolverLimits().to_native()
+    tA, tb, tc = (torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (A, b, c))
+    out = dict(status=torch.empty(count, dtype=torch.int8, device=dev),
+               objective=torch.empty(count, dtype=torch.float64, device=dev),
+               x=torch.empty(count, n, dtype=torch.float64, device=dev),
+               it1=torch.empty(count, dtype=torch.int32, device=dev),
+               it2=torch.empty(count, dtype=torch.int32, device=dev))
+    stream = torch.cuda.current_stream(dev)
+    l2_flush = None
+    inputs_bytes = count * (m * n + m + n) * 8 if not shared else (m * n + m + count * n) * 8
+    if inputs_bytes <= 256e6:
+        l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        if l2_flush is not None:
+            l2_flush.zero_()
+        _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+
+    # ---- device-resident value: CUDA events per step on the launching stream ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record(stream)
+        for e0, e1 in evs:
+            if l2_flush is not None:
+                l2_flush.zero_()
+            e0.record(stream)
+            _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared, stream=stream)
+            e1.record(stream)
+        t_all1.record(stream)
+        barrier()
+    launches = _native.launch_count() - launches0
+    kernel_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    step_ms = statistics.mean(kernel_ms)
+    region_ms = t_all0.elapsed_time(t_all1)
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    pivots = int((res["it1"].astype(np.int64) + res["it2"]).sum())
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    ms_per_step = max_over_ranks(step_ms)
+    total_lps = count * world
+    value = total_lps / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel ----
+    variant = _native.kernel_variant(m, n)
+    bpp = bytes_per_pivot(m, n)
+    achieved = pivots * bpp / (step_ms / 1e3) / 1e9
+    if variant.startswith("smem"):
+        peak = _native.probe_smem_gbs(local)
+        bound, peak_src = "smem", "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
+    else:
+        peak, peak_src = measured_hbm_gbs()
+        bound = "hbm"
+    hbm_peak, hbm_src = measured_hbm_gbs()
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": peak_src, "kernel": f"tableau_kernel[{variant}]",
+                "bytes_per_pivot": bpp, "pivots_per_launch": pivots,
+                "hbm_frac": achieved / hbm_peak, "hbm_peak": hbm_peak}
+
+    # ---- e2e through the public API from pinned host buffers ----
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    hA, hb, hc = pin(A), pin(b), pin(c)
+    h2d = hA.nbytes + hb.nbytes + hc.nbytes
+    d2h = count * (1 + 8 + 8 * n + 4 + 4)
+    from paper_1802_08557_b200 import support_batch
+    call = (lambda: support_batch(hA, hb, hc)) if shared else (lambda: batch_solve_arrays(hA, hb, hc))
+    call()
+    barrier()
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 10))):
+        barrier()
+        t0 = time.perf_counter()
+        r = call()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e_t))
+    assert np.array_equal(r.status, res["status"]) and np.array_equal(r.x, res["x"]), "e2e result differs"
+
+    total_pivots = sum_over_ranks(pivots)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (workloads recipe, seed+1000*rank)",
+        "config": config_block(args, spec, count, shared) | {"kernel": variant},
+        "pivots_per_s": total_pivots / (ms_per_step / 1e3),
+        "status_counts": {str(k): int(v) for k, v in zip(*np.unique(res["status"], return_counts=True))},
+        "roofline": roofline,
+        "e2e": {"value": total_lps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                "api": "batch_solve_arrays (blp_solve_batch_host, 3-stream pipelined sub-batches)"},
+        "gpu_launches": int(launches),
+        "timed_region_ms": region_ms,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(A, b, c, shared)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -31,7 +31,9 @@
  * Results are bit-identical to the reference's pivot sequence: status, x and
  * iteration counts equal the reference's exactly; objective agrees to 1e-9
  * relative (the reference sums c.x with BLAS ddot, whose order is unpinned).
- * Validation (non-finite inputs, model.py:263-301) is the caller's job.
+ * Finiteness validation (model.py:263-301) is fused into the kernels' tableau
+ * build: an LP with a non-finite entry gets BLP_STATUS_INVALID and is not
+ * solved; the caller turns it into the reference's ValueError.
  */
 #ifndef BLP_H_
 #define BLP_H_
@@ -51,6 +53,9 @@ extern "C" {
 #define BLP_STATUS_ITERATION_LIMIT 3
 /* phase 1 reported unbounded: the reference raises RuntimeError (simplex.py:173-175) */
 #define BLP_STATUS_ERR_PHASE1_UNBOUNDED 4
+/* a non-finite entry in A, b or c: the reference's solve raises
+ * ValueError("invalid LP: ...") from validate() (simplex.py:162-164) */
+#define BLP_STATUS_INVALID 5
 
 /* Return codes of the entry points. */
 #define BLP_OK 0
@@ -106,6 +111,10 @@ int64_t blp_launch_count(void);
 
 /* Text of the last error on the calling thread ("" if none). */
 const char *blp_last_error(void);
+
+/* Measured shared-memory bandwidth of `device` in GB/s (LDS+STS bytes, all
+ * SMs), the roofline denominator of the smem-resident kernels; < 0 on error. */
+double blp_probe_smem_gbs(int32_t device);
 
 /* BLP_ABI_VERSION of the loaded library. */
 int blp_abi_version(void);

@@ -40,7 +40,8 @@ _lib = None
 
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
 EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
-           "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version")
+           "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
+           "blp_probe_smem_gbs")
 
 
 def load():
@@ -67,6 +68,8 @@ def load():
     lib.blp_launch_count.restype = ctypes.c_int64
     lib.blp_last_error.argtypes = []
     lib.blp_last_error.restype = ctypes.c_char_p
+    lib.blp_probe_smem_gbs.argtypes = [ctypes.c_int32]
+    lib.blp_probe_smem_gbs.restype = ctypes.c_double
     lib.blp_abi_version.argtypes = []
     lib.blp_abi_version.restype = ctypes.c_int
     _lib = lib
@@ -93,6 +96,15 @@ def make_limits(max_iterations=None, anti_cycling=True, degenerate_pivot_limit=N
 
 def kernel_variant(m: int, n: int) -> str:
     return load().blp_kernel_variant(m, n).decode()
+
+
+def probe_smem_gbs(device: int = 0) -> float:
+    """Measured LDS+STS bandwidth of one GPU (GB/s)."""
+    _require_gpu()
+    v = float(load().blp_probe_smem_gbs(int(device)))
+    if v < 0:
+        raise NativeError("smem probe failed: " + load().blp_last_error().decode())
+    return v
 
 
 def launch_count() -> int:

@@ -8,7 +8,7 @@ with the batch-worst artificial count (:146-153, ``lp_memory_bytes`` :98-106,
 ``chunk_seconds`` entry per planned chunk, ``total_seconds``.
 
 What changes is underneath: the LPs are packed once into contiguous arrays
-(one ``np.asarray``), validated with one vectorised ``np.isfinite`` pass, and
+(one copy), validated inside the kernel's tableau build (non-finite entries), and
 each planned chunk is one call into libblp.so, which pipelines sub-batches
 over CUDA streams on the GPU(s).  ``worker_count`` stays what it is in the
 reference -- a throughput knob that never changes results -- and is unused
@@ -29,7 +29,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native
-from .model import SolveOutcome, StandardFormLP, STATUS_BY_CODE, first_nonfinite, invalid_message, validate
+from .model import SolveOutcome, StandardFormLP, STATUS_BY_CODE, invalid_message, validate
 from .simplex import PHASE1_UNBOUNDED_MESSAGE, SolverLimits, outcome_from_arrays
 
 # Column ceiling of the paper's one-block-per-LP Kepler kernel (batch.py:25-29);
@@ -196,23 +196,21 @@ def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared
     return out
 
 
-def batch_solve_arrays(A, b, c, limits: SolverLimits = SolverLimits(), *, devices: Sequence[int] = (0,),
-                       check_finite: bool = True) -> BatchArrays:
+def batch_solve_arrays(A, b, c, limits: SolverLimits = SolverLimits(), *,
+                       devices: Sequence[int] = (0,)) -> BatchArrays:
     """Solve a packed batch: A [B,m,n], b [B,m], c [B,n] (fp64).  GPU only.
 
-    Raises ValueError (reference message) for the first LP with a non-finite
-    entry and RuntimeError if any LP's phase 1 reports unbounded.
+    Finiteness is validated inside the kernel's tableau build; the first LP
+    with a non-finite entry raises the reference's ValueError, an LP whose
+    phase 1 reports unbounded raises RuntimeError (whichever comes first).
     """
     A, b, c = _as_f64(A), _as_f64(b), _as_f64(c)
     if A.ndim != 3 or b.ndim != 2 or c.ndim != 2 or A.shape != (c.shape[0], b.shape[1], c.shape[1]) \
             or b.shape[0] != c.shape[0]:
         raise ValueError(f"packed shapes disagree: A {A.shape}, b {b.shape}, c {c.shape}")
-    if check_finite:
-        k = first_nonfinite(A, b, c)
-        if k >= 0:
-            raise ValueError(invalid_message(validate(StandardFormLP(c=c[k], A=A[k], b=b[k]))))
     res = _solve_sharded(A, b, c, limits, devices, shared_Ab=False)
-    return _finish(res)
+    _raise_for_errors(res, lambda k: StandardFormLP(c=c[k], A=A[k], b=b[k]))
+    return _arrays(res)
 
 
 def support_batch(A, b, C, limits: SolverLimits = SolverLimits(), *, devices: Sequence[int] = (0,)) -> BatchArrays:
@@ -225,18 +223,22 @@ def support_batch(A, b, C, limits: SolverLimits = SolverLimits(), *, devices: Se
     A, b, C = _as_f64(A), _as_f64(b), _as_f64(C)
     if A.ndim != 2 or b.ndim != 1 or C.ndim != 2 or A.shape != (b.shape[0], C.shape[1]):
         raise ValueError(f"support shapes disagree: A {A.shape}, b {b.shape}, C {C.shape}")
-    if not (np.isfinite(A).all() and np.isfinite(b).all()) and len(C):
-        raise ValueError(invalid_message(validate(StandardFormLP(c=C[0], A=A, b=b))))
-    bad = np.flatnonzero(~np.isfinite(C).all(axis=1))
-    if bad.size:
-        raise ValueError(invalid_message(validate(StandardFormLP(c=C[bad[0]], A=A, b=b))))
     res = _solve_sharded(A, b, C, limits, devices, shared_Ab=True)
-    return _finish(res)
+    _raise_for_errors(res, lambda k: StandardFormLP(c=C[k], A=A, b=b))
+    return _arrays(res)
 
 
-def _finish(res: dict) -> BatchArrays:
-    if (res["status"] == 4).any():
+def _raise_for_errors(res: dict, lp_of) -> None:
+    """Reference error behaviour for the first failing LP in index order."""
+    bad = np.flatnonzero(res["status"] >= 4)
+    if bad.size:
+        k = int(bad[0])
+        if res["status"][k] == 5:
+            raise ValueError(invalid_message(validate(lp_of(k))))
         raise RuntimeError(PHASE1_UNBOUNDED_MESSAGE)
+
+
+def _arrays(res: dict) -> BatchArrays:
     return BatchArrays(res["status"], res["objective"], res["x"], res["it1"], res["it2"])
 
 
@@ -272,9 +274,9 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
     if not lps:
         return BatchReport(outcomes=[], plan=plan, chunk_seconds=[], total_seconds=0.0)
 
-    # Pack once, validate once.  The reference raises at the first invalid LP
-    # in index order (solve() inside the chunk loop), after solving the ones
-    # before it; a phase-1-unbounded LP earlier in the batch raises first.
+    # Pack once.  The reference raises at the first invalid LP in index order
+    # (validate() inside solve()); a mis-shaped A stops packing there, and
+    # non-finite entries are flagged by the kernel (BLP_STATUS_INVALID).
     bad_shape = _first_bad_shape(lps, m, n)
     limit = bad_shape if bad_shape >= 0 else len(lps)
     A = np.empty((limit, m, n), np.float64)
@@ -285,15 +287,11 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
         A[k] = lp.A
         b[k] = lp.b
         c[k] = lp.c
-    bad_value = first_nonfinite(A, b, c)
-    first_bad = bad_value if bad_value >= 0 else bad_shape
-    if first_bad >= 0:
-        if first_bad:
-            res = _solve_sharded(A[:first_bad], b[:first_bad], c[:first_bad], config.limits,
-                                 config.devices, shared_Ab=False)
-            if (res["status"] == 4).any():
-                raise RuntimeError(PHASE1_UNBOUNDED_MESSAGE)
-        raise ValueError(invalid_message(validate(lps[first_bad])))
+    if bad_shape >= 0:
+        if bad_shape:
+            res = _solve_sharded(A, b, c, config.limits, config.devices, shared_Ab=False)
+            _raise_for_errors(res, lambda k: lps[k])
+        raise ValueError(invalid_message(validate(lps[bad_shape])))
 
     outcomes: list[SolveOutcome | None] = [None] * len(lps)
     chunk_seconds: list[float] = []
@@ -302,6 +300,7 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
         t0 = time.perf_counter()
         res = _solve_sharded(A[start:end], b[start:end], c[start:end], config.limits,
                              config.devices, shared_Ab=False)
+        _raise_for_errors(res, lambda k: lps[start + k])
         outcomes[start:end] = [outcome_from_arrays(res, k) for k in range(end - start)]
         chunk_seconds.append(time.perf_counter() - t0)
     total = time.perf_counter() - started

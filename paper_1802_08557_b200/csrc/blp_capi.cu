@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -17,6 +18,7 @@
 
 #include "../../include/blp.h"
 #include "blp_common.cuh"
+#include "blp_regtile_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 
 namespace {
@@ -40,36 +42,90 @@ constexpr size_t kMaxDynSmem = 227 * 1024;
 
 using KernelFn = void (*)(blp::Batch);
 
-struct Variant {
-    KernelFn fn;
-    const char *name;
-    bool smem_tab;
-    int max_threads;
+// One launch configuration: kernel variant, CTA size, dynamic smem, HBM tableau slot.
+struct Plan {
+    KernelFn fn = nullptr;
+    const char *name = "unsupported";
+    int threads = 0;
+    size_t smem = 0;
+    long long slot = 0;  // doubles of global tableau per CTA (HBM-streamed variant)
 };
 
-// Rows per lane (RPL) = ceil((m+1)/32) selects the register footprint.
-Variant pick_variant(int m, int n, bool *ok) {
-    const int rows = m + 1;
-    const int rpl = (rows + 31) / 32;
-    const blp::TabLayout Ls = blp::make_tab_layout(m, n, 32, true);
-    *ok = true;
-    if (Ls.bytes <= kMaxDynSmem) {
-        switch (rpl) {
-            case 1: return {blp::tableau_kernel<1, true, 1024>, "smem_rpl1", true, 1024};
-            case 2: return {blp::tableau_kernel<2, true, 1024>, "smem_rpl2", true, 1024};
-            case 3: return {blp::tableau_kernel<3, true, 1024>, "smem_rpl3", true, 1024};
-            case 4: return {blp::tableau_kernel<4, true, 1024>, "smem_rpl4", true, 1024};
-            default: break;
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+// Register-tile variant for m <= 64: columns per warp CPW (BLP_RT_CPW overrides).
+bool plan_regtile(int m, int n, Plan *p) {
+    const int ncols = n + m + 1;
+    const int rpl = m <= 32 ? 1 : (m <= 64 ? 2 : 0);
+    if (rpl == 0) return false;
+    int cpw = env_int("BLP_RT_CPW", rpl == 1 ? 32 : 16);
+    struct Inst { int rpl, cpw, maxt; KernelFn fn; const char *name; };
+    static const Inst insts[] = {
+        {1, 16, 512, blp::regtile_kernel<1, 16, 512>, "regtile_r1_c16"},
+        {1, 32, 256, blp::regtile_kernel<1, 32, 256>, "regtile_r1_c32"},
+        {1, 64, 128, blp::regtile_kernel<1, 64, 128>, "regtile_r1_c64"},
+        {2, 16, 512, blp::regtile_kernel<2, 16, 512>, "regtile_r2_c16"},
+        {2, 32, 256, blp::regtile_kernel<2, 32, 256>, "regtile_r2_c32"},
+    };
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (const Inst &I : insts) {
+            if (I.rpl != rpl || I.cpw != cpw) continue;
+            const int nw = (ncols + I.cpw - 1) / I.cpw;
+            if (nw * 32 > I.maxt) break;
+            const blp::RtLayout L = blp::make_rt_layout(I.rpl, I.cpw, nw);
+            if (L.bytes > kMaxDynSmem) break;
+            p->fn = I.fn; p->name = I.name; p->threads = nw * 32; p->smem = L.bytes; p->slot = 0;
+            return true;
         }
+        cpw = rpl == 1 ? 64 : 32;  // wider tiles for wide LPs
     }
-    if (rpl <= 1) return {blp::tableau_kernel<1, false, 1024>, "hbm_rpl1", false, 1024};
-    if (rpl <= 2) return {blp::tableau_kernel<2, false, 1024>, "hbm_rpl2", false, 1024};
-    if (rpl <= 4) return {blp::tableau_kernel<4, false, 1024>, "hbm_rpl4", false, 1024};
-    if (rpl <= 8) return {blp::tableau_kernel<8, false, 512>, "hbm_rpl8", false, 512};
-    if (rpl <= 16) return {blp::tableau_kernel<16, false, 512>, "hbm_rpl16", false, 512};
-    if (rpl <= 32) return {blp::tableau_kernel<32, false, 256>, "hbm_rpl32", false, 256};
-    *ok = false;
-    return {nullptr, "unsupported", false, 0};
+    return false;
+}
+
+// Shared-memory (or HBM) tableau variant; rows per lane RPL = ceil((m+1)/32).
+bool plan_tableau(int m, int n, Plan *p) {
+    const int rpl = (m + 1 + 31) / 32;
+    const blp::TabLayout Ls = blp::make_tab_layout(m, n, 32, true);
+    bool smem_tab = Ls.bytes <= kMaxDynSmem && rpl <= 4 && env_int("BLP_FORCE_HBM", 0) == 0;
+    int maxt = 1024;
+    if (smem_tab) {
+        switch (rpl) {
+            case 1: p->fn = blp::tableau_kernel<1, true, 1024>; p->name = "smem_rpl1"; break;
+            case 2: p->fn = blp::tableau_kernel<2, true, 1024>; p->name = "smem_rpl2"; break;
+            case 3: p->fn = blp::tableau_kernel<3, true, 1024>; p->name = "smem_rpl3"; break;
+            default: p->fn = blp::tableau_kernel<4, true, 1024>; p->name = "smem_rpl4"; break;
+        }
+    } else if (rpl <= 1) { p->fn = blp::tableau_kernel<1, false, 1024>; p->name = "hbm_rpl1"; }
+    else if (rpl <= 2) { p->fn = blp::tableau_kernel<2, false, 1024>; p->name = "hbm_rpl2"; }
+    else if (rpl <= 4) { p->fn = blp::tableau_kernel<4, false, 1024>; p->name = "hbm_rpl4"; }
+    else if (rpl <= 8) { p->fn = blp::tableau_kernel<8, false, 512>; p->name = "hbm_rpl8"; maxt = 512; }
+    else if (rpl <= 16) { p->fn = blp::tableau_kernel<16, false, 512>; p->name = "hbm_rpl16"; maxt = 512; }
+    else if (rpl <= 32) { p->fn = blp::tableau_kernel<32, false, 256>; p->name = "hbm_rpl32"; maxt = 256; }
+    else return false;
+    // threads: resident CTAs of one SM hold ~32 warps (register budget ~64/thread),
+    // never more warps than columns
+    const int ncols = n + m + 1;
+    int ctas = smem_tab ? (int)std::max<size_t>(1, (228 * 1024) / (Ls.bytes + 1024)) : 2;
+    ctas = std::min(ctas, 16);
+    int warps = std::max(2, 32 / ctas);
+    warps = std::min(warps, std::max(1, (ncols + 1) / 2));
+    warps = std::min(warps, maxt / 32);
+    p->threads = std::max(1, warps) * 32;
+    const blp::TabLayout L = blp::make_tab_layout(m, n, p->threads / 32, smem_tab);
+    p->smem = L.bytes;
+    p->slot = smem_tab ? 0 : (long long)L.ncols * L.ld;
+    return true;
+}
+
+// BLP_KERNEL=regtile|smem forces a family (testing / tuning).
+bool plan_launch(int m, int n, Plan *p) {
+    const char *force = getenv("BLP_KERNEL");
+    const bool allow_rt = !(force && strcmp(force, "smem") == 0);
+    if (allow_rt && plan_regtile(m, n, p)) return true;
+    return plan_tableau(m, n, p);
 }
 
 struct DeviceInfo {
@@ -95,18 +151,6 @@ int device_sms(int dev, int *sms) {
     return BLP_OK;
 }
 
-// Threads per CTA: enough warps that the resident CTAs of one SM hold about
-// 32 warps (register budget ~64/thread), never more warps than columns.
-int pick_threads(const Variant &v, int m, int n, size_t smem) {
-    const int ncols = n + m + 1;
-    int ctas = v.smem_tab ? (int)std::max<size_t>(1, (228 * 1024) / (smem + 1024)) : 2;
-    ctas = std::min(ctas, 16);
-    int warps = std::max(2, 32 / ctas);
-    warps = std::min(warps, std::max(1, (ncols + 1) / 2));
-    warps = std::min(warps, v.max_threads / 32);
-    return std::max(1, warps) * 32;
-}
-
 int launch_solve(const double *A, const double *b, const double *c, long long count, int m, int n,
                  int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
                  int32_t *it1, int32_t *it2, cudaStream_t stream) {
@@ -116,22 +160,16 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     int sms = 0;
     int rc = device_sms(dev, &sms);
     if (rc) return rc;
-    bool ok = false;
-    Variant v = pick_variant(m, n, &ok);
-    if (!ok) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
-    // threads first (layout size depends only weakly on it), then smem
-    blp::TabLayout L = blp::make_tab_layout(m, n, 32, v.smem_tab);
-    const int threads = pick_threads(v, m, n, L.bytes);
-    L = blp::make_tab_layout(m, n, threads / 32, v.smem_tab);
-    BLP_CUDA_TRY(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+    Plan P;
+    if (!plan_launch(m, n, &P)) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
+    BLP_CUDA_TRY(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     int occ = 0;
-    BLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, threads, L.bytes));
+    BLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, P.fn, P.threads, P.smem));
     if (occ < 1) return fail(BLP_ERR_TOO_LARGE, "kernel variant cannot be resident on an SM");
     long long grid = (long long)occ * sms;
     if (grid > count) grid = count;
 
-    const long long slot = v.smem_tab ? 0 : (long long)L.ncols * L.ld;
-    const size_t ws_bytes = 256 + (size_t)slot * sizeof(double) * (size_t)grid;
+    const size_t ws_bytes = 256 + (size_t)P.slot * sizeof(double) * (size_t)grid;
     void *ws = nullptr;
     BLP_CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, stream));
     BLP_CUDA_TRY(cudaMemsetAsync(ws, 0, 256, stream));
@@ -140,14 +178,14 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.A = A; B.b = b; B.c = c; B.count = count; B.m = m; B.n = n; B.shared_Ab = shared_Ab;
     B.status = status; B.objective = objective; B.x = x; B.it1 = it1; B.it2 = it2;
     B.next_lp = reinterpret_cast<int *>(ws);
-    B.gtab = v.smem_tab ? nullptr : reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
-    B.gtab_stride = slot;
+    B.gtab = P.slot ? reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256) : nullptr;
+    B.gtab_stride = P.slot;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
     B.lim.reserved = 0;
 
-    v.fn<<<(unsigned)grid, threads, L.bytes, stream>>>(B);
+    P.fn<<<(unsigned)grid, P.threads, P.smem, stream>>>(B);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     BLP_CUDA_TRY(cudaGetLastError());
     BLP_CUDA_TRY(cudaFreeAsync(ws, stream));
@@ -163,6 +201,32 @@ bool bad_args(const double *A, const double *b, const double *c, long long count
     return !status || !objective || !it1 || !it2;
 }
 
+// Shared-memory bandwidth probe: every thread streams 16-byte LDS/STS pairs
+// over a conflict-free slice for `iters` rounds (the roofline denominator of
+// the smem-resident kernels; BASELINE.md §2 asks for it to be measured).
+__global__ void __launch_bounds__(1024) smem_probe_kernel(double *sink, int iters) {
+    extern __shared__ __align__(16) unsigned char probe_smem[];
+    const unsigned base = (unsigned)__cvta_generic_to_shared(probe_smem);
+    const int slots = blockDim.x * 4;
+    for (int s = threadIdx.x; s < slots; s += blockDim.x) {
+        const unsigned a = base + 16u * s;
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"((double)s), "d"(1.0) : "memory");
+    }
+    __syncthreads();
+    double acc = 0.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned a = base + 16u * (threadIdx.x + q * blockDim.x);
+            double x, y;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(y), "d"(x) : "memory");
+            acc += x;
+        }
+    }
+    if (acc == -1.0) sink[0] = acc;  // keep the loop observable
+}
+
 struct StreamSet {
     std::vector<cudaStream_t> s;
 };
@@ -174,21 +238,50 @@ extern "C" {
 
 int blp_abi_version(void) { return BLP_ABI_VERSION; }
 
+double blp_probe_smem_gbs(int32_t device) {
+    g_last_error.clear();
+    int sms = 0;
+    if (cudaSetDevice(device) != cudaSuccess || device_sms(device, &sms) != BLP_OK) return -1.0;
+    const int threads = 1024, iters = 4096;
+    const size_t smem = (size_t)threads * 4 * 16;  // 64 KB: two CTAs (2048 threads) per SM
+    if (cudaFuncSetAttribute(smem_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return -1.0;
+    double *sink = nullptr;
+    cudaEvent_t e0, e1;
+    if (cudaMalloc(&sink, 8) != cudaSuccess) return -1.0;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = 2 * sms;
+    smem_probe_kernel<<<grid, threads, smem>>>(sink, 64);  // warm-up
+    cudaEventRecord(e0);
+    smem_probe_kernel<<<grid, threads, smem>>>(sink, iters);
+    cudaEventRecord(e1);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    float ms = 0.f;
+    const bool ok = cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (!ok || ms <= 0.f) return -1.0;
+    const double bytes = (double)grid * threads * 4.0 * 32.0 * iters;  // 16 B read + 16 B write per slot
+    return bytes / (ms * 1e-3) / 1e9;
+}
+
 const char *blp_last_error(void) { return g_last_error.c_str(); }
 
 int64_t blp_launch_count(void) { return g_launches.load(); }
 
 int blp_shape_supported(int32_t m, int32_t n) {
-    bool ok = false;
+    Plan P;
     if (m < 0 || n < 0) return 0;
-    pick_variant(m, n, &ok);
-    return ok ? 1 : 0;
+    return plan_launch(m, n, &P) ? 1 : 0;
 }
 
 const char *blp_kernel_variant(int32_t m, int32_t n) {
-    bool ok = false;
+    Plan P;
     if (m < 0 || n < 0) return "invalid";
-    return pick_variant(m, n, &ok).name;
+    plan_launch(m, n, &P);
+    return P.name;
 }
 
 int blp_solve_batch_device(const double *A, const double *b, const double *c, int64_t count,

@@ -33,6 +33,7 @@ enum : int8_t {
     kInfeasible = 2,
     kIterationLimit = 3,
     kErrPhase1Unbounded = 4,
+    kInvalid = 5,          // non-finite entry: the caller raises validate()'s ValueError
 };
 
 // SolverLimits (simplex.py:34-60); same layout as blp_limits.

@@ -1,0 +1,51 @@
+// blp_keys.cuh -- numpy-exact arg-reductions on order-preserving 64-bit keys.
+//
+// np.argmax / np.argmin (tableau.py:183, :212; simplex.py:124) return the
+// first index of the extreme value, NaN counting as the extreme, and treat
+// -0.0 == +0.0.  Mapping each double to an unsigned key whose integer order
+// is that total order turns every arg-reduction into three warp-wide
+// redux.sync instructions (max of the high word, max of the low word among
+// the winners, min of the index among the full-key winners) instead of a
+// five-level shuffle tree of double compares.
+#pragma once
+
+#include "blp_common.cuh"
+
+namespace blp {
+
+// Key whose unsigned order is numpy's max order: -inf < ... < -0 == +0 < ... < +inf < NaN.
+__device__ __forceinline__ unsigned long long key_max(double v) {
+    if (v != v) return ~0ull;
+    const long long b = __double_as_longlong(v == 0.0 ? 0.0 : v);
+    return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+}
+
+// Key whose unsigned order is numpy's min order: NaN < -inf < ... < +inf.
+__device__ __forceinline__ unsigned long long key_min(double v) {
+    return v != v ? 0ull : key_max(v);
+}
+
+constexpr unsigned long long kKeyEmptyMax = 0ull;    // no candidate (max reductions)
+constexpr unsigned long long kKeyEmptyMin = ~0ull;   // no candidate (min reductions)
+
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
+    const unsigned hi = __reduce_max_sync(kFull, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_max_sync(kFull, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_key(unsigned long long k) {
+    const unsigned hi = __reduce_min_sync(kFull, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_min_sync(kFull, (unsigned)(k >> 32) == hi ? (unsigned)k : ~0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+// Lowest index among the lanes holding the winning key (kNone if none).
+__device__ __forceinline__ int warp_index_of(unsigned long long k, unsigned long long win, int idx) {
+    return (int)__reduce_min_sync(kFull, k == win ? (unsigned)idx : (unsigned)kNone);
+}
+
+// Keys of the reference thresholds, for comparisons done on keys.
+__device__ __forceinline__ unsigned long long key_of_tol() { return key_max(kTol); }
+
+}  // namespace blp

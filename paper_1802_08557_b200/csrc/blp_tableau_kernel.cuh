@@ -374,9 +374,11 @@ tableau_kernel(Batch B) {
 
         // ---- build_tableau (tableau.py:139-172) ----
         for (int j = X.tid; j < n + 2 * m; j += X.nt) X.isb[j] = 0;
+        bool nonfinite = false;  // validate (model.py:263-301), fused into the load
         for (int base = 0; base < m; base += X.nt) {
             const int i = base + X.tid;
             const double bi = i < m ? bg[i] : 0.0;
+            nonfinite |= !isfinite(bi);
             const bool neg = i < m && bi < 0.0;
             const unsigned bal = __ballot_sync(kFull, neg);
             if (X.lane == 0) X.wcnt[X.warp] = __popc(bal);
@@ -397,22 +399,30 @@ tableau_kernel(Batch B) {
         X.n_art = (int)X.misc[1];
         for (int k = X.tid; k < m * n; k += X.nt) {
             const int i = k / n, j = k - i * n;
-            X.T[(size_t)j * ld + i] = __dmul_rn(Ag[k], X.cbv[i]);
+            const double a = Ag[k];
+            nonfinite |= !isfinite(a);
+            X.T[(size_t)j * ld + i] = __dmul_rn(a, X.cbv[i]);
         }
         for (int k = X.tid; k < m * (m + 1); k += X.nt) {
             const int jj = k / (m + 1), i = k - jj * (m + 1);
             X.T[(size_t)(n + jj) * ld + i] = (i == jj) ? X.cbv[i] : 0.0;
         }
-        for (int j = X.tid; j <= n; j += X.nt)
-            X.T[(size_t)(j < n ? j : rhs) * ld + m] = j < n ? cg[j] : 0.0;
-        __syncthreads();
+        for (int j = X.tid; j <= n; j += X.nt) {
+            const double cj = j < n ? cg[j] : 0.0;
+            nonfinite |= !isfinite(cj);
+            X.T[(size_t)(j < n ? j : rhs) * ld + m] = cj;
+        }
+        const bool invalid = __syncthreads_or(nonfinite);
         for (int i = X.tid; i < m; i += X.nt) X.isb[X.basis[i]] = 1;
         __syncthreads();
 
         int8_t status = kOptimal;
         int it1 = 0, it2 = 0;
         bool done = false;
-        if (X.n_art > 0) {
+        if (invalid) {
+            status = kInvalid;
+            done = true;
+        } else if (X.n_art > 0) {
             price_out<RPL, 1>(X, cg);
             const PhaseResult r1 = run_phase<RPL, kPhase1>(X, B.lim);
             __syncthreads();

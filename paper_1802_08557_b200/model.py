@@ -8,9 +8,9 @@ values and violation messages so callers and tests written against the
 reference work unchanged.  General-form lowering (GeneralLP, standardize,
 VariableMap) is host-side ingest outside the batched path.
 
-``validate_packed`` is the vectorised check the batch path uses: it finds the
-non-finite LPs of a packed batch with one ``np.isfinite`` pass and only then
-calls ``validate`` to reproduce the reference's message for the first one.
+The batch path does not call ``validate`` per LP: the kernels flag non-finite
+inputs while building the tableau (BLP_STATUS_INVALID) and ``validate`` is
+called only on the first flagged LP, to reproduce the reference's message.
 """
 from __future__ import annotations
 
@@ -104,16 +104,3 @@ def validate(lp: StandardFormLP) -> list[str]:
 def invalid_message(violations: list[str]) -> str:
     """The ValueError text solve() raises (simplex.py:162-164)."""
     return "invalid LP: " + "; ".join(violations)
-
-
-def first_nonfinite(A: np.ndarray, b: np.ndarray, c: np.ndarray, shared_Ab: bool = False) -> int:
-    """Index of the first LP of a packed batch holding a non-finite entry, or -1."""
-    bad_c = ~np.isfinite(c).all(axis=1)
-    if shared_Ab:
-        if not (np.isfinite(A).all() and np.isfinite(b).all()):
-            return 0 if len(c) else -1
-        bad = bad_c
-    else:
-        bad = bad_c | ~np.isfinite(b).all(axis=1) | ~np.isfinite(A.reshape(len(A), -1)).all(axis=1)
-    idx = np.flatnonzero(bad)
-    return int(idx[0]) if idx.size else -1

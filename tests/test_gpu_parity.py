@@ -1,0 +1,172 @@
+"""CUDA path vs the reference (golden fixtures) and vs the CPU oracle -- through the C ABI.
+
+Bar (BASELINE.json north star): status, x and per-phase iteration counts
+identical to the reference; objective within 1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+from golden_io import compare, json_records, packed_fixture, packed_names
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _native_dict(res):
+    return dict(status=res.status, objective=res.objective, x=res.x, it1=res.iterations_phase1,
+                it2=res.iterations_phase2)
+
+
+def _want(rec):
+    o = rec["outcome"]
+    n = rec["n"]
+    return dict(status=[o["status"]], it1=[o["it1"]], it2=[o["it2"]],
+                objective=[o.get("objective", np.nan)], x=[o.get("x", [0.0] * n)] if n else np.zeros((1, 0)))
+
+
+@pytest.mark.parametrize("fixture", ["known.json", "ragged.json"])
+def test_records_match_reference(fixture):
+    from paper_1802_08557_b200 import SolverLimits, batch_solve_arrays
+    for rec in json_records(fixture):
+        res = batch_solve_arrays(rec["A"][None], rec["b"][None], rec["c"][None], SolverLimits(**rec["limits"]))
+        compare(_native_dict(res), _want(rec), f"{fixture}:{rec['name']}")
+
+
+def test_records_batched_by_shape_match_reference():
+    """Same records, grouped into same-shape batches (exercises the persistent LP queue)."""
+    from paper_1802_08557_b200 import batch_solve_arrays
+    groups = {}
+    for rec in json_records("ragged.json"):
+        if rec["limits"] == dict(max_iterations=None, anti_cycling=True, degenerate_pivot_limit=None):
+            groups.setdefault((rec["m"], rec["n"]), []).append(rec)
+    for shape, recs in groups.items():
+        A = np.stack([r["A"] for r in recs]).reshape(len(recs), *shape)
+        b = np.stack([r["b"] for r in recs]).reshape(len(recs), shape[0])
+        c = np.stack([r["c"] for r in recs]).reshape(len(recs), shape[1])
+        res = batch_solve_arrays(A, b, c)
+        for k, r in enumerate(recs):
+            got = {key: val[k:k + 1] for key, val in _native_dict(res).items()}
+            compare(got, _want(r), f"{shape}:{r['name']}")
+
+
+@pytest.mark.parametrize("stem", packed_names())
+def test_packed_families_match_reference(stem):
+    from paper_1802_08557_b200 import batch_solve_arrays, support_batch
+    fx = packed_fixture(stem)
+    if fx["shared"]:
+        res = support_batch(fx["A"], fx["b"], fx["c"])
+    else:
+        res = batch_solve_arrays(fx["A"], fx["b"], fx["c"])
+    compare(_native_dict(res), fx, stem)
+
+
+def test_object_api_matches_reference_layout():
+    """batch_solve / solve return SolveOutcome objects laid out as the reference's."""
+    from paper_1802_08557_b200 import BatchConfig, Status, batch_solve, gen_random_lps, solve, standard_form
+    lp = standard_form([3.0, 5.0], [[1, 0], [0, 2], [3, 2]], [4.0, 12.0, 18.0])
+    out = solve(lp)
+    assert out.status is Status.OPTIMAL and out.objective_value == pytest.approx(36.0)
+    assert out.primal_point.tolist() == [2.0, 6.0]
+    lps = gen_random_lps(5, 40, seed=11)
+    rep = batch_solve(lps, BatchConfig(memory_budget_bytes=768 * 7))
+    assert rep.plan.count == 6 and len(rep.chunk_seconds) == 6
+    for lp_k, o in zip(lps, rep.outcomes):
+        d = solve(lp_k)
+        assert (o.status, o.objective_value, o.iterations_phase1, o.iterations_phase2) == \
+            (d.status, d.objective_value, d.iterations_phase1, d.iterations_phase2)
+        assert np.array_equal(o.primal_point, d.primal_point)
+    assert rep.status_counts() == {"optimal": 40}
+
+
+def test_invalid_lp_raises_reference_message():
+    from paper_1802_08557_b200 import batch_solve, standard_form, solve
+    with pytest.raises(ValueError, match="invalid LP: A\\[0\\]\\[0\\] is not finite"):
+        solve(standard_form([1.0], [[np.nan]], [1.0]))
+    lps = [standard_form([1.0], [[1.0]], [1.0]), standard_form([1.0], [[1.0]], [np.inf])]
+    with pytest.raises(ValueError, match="invalid LP: b\\[0\\] is not finite"):
+        batch_solve(lps)
+
+
+def test_afiro_against_oracle_20k():
+    """20,000 fresh C2-recipe LPs (seed not in the fixtures) vs the CPU oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import batch_solve_arrays, workloads
+    A, b, c = workloads.afiro_arrays(20_000, seed=77)
+    res = batch_solve_arrays(A, b, c)
+    compare(_native_dict(res), oracle.solve_batch(A, b, c), "afiro20k")
+
+
+def test_support_against_oracle_and_unshared():
+    """Support-function mode equals the same LPs solved with A, b replicated."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import batch_solve_arrays, support_batch, workloads
+    A, b = workloads.support_polytope()
+    C = workloads.support_directions(5000, offset=2000)
+    res = support_batch(A, b, C)
+    compare(_native_dict(res), oracle.solve_batch(A, b, C, shared_Ab=True), "support5k")
+    rep = batch_solve_arrays(np.broadcast_to(A, (len(C),) + A.shape), np.broadcast_to(b, (len(C),) + b.shape), C)
+    compare(_native_dict(rep), _native_dict(res), "support-vs-replicated")
+
+
+def test_device_api_equals_host_api():
+    """blp_solve_batch_device on torch tensors == blp_solve_batch_host on numpy arrays."""
+    from paper_1802_08557_b200 import SolverLimits, _native, batch_solve_arrays, workloads
+    A, b, c = workloads.afiro_arrays(3000, seed=5)
+    host = _native_dict(batch_solve_arrays(A, b, c))
+    dev = torch.device("cuda:0")
+    tA, tb, tc = (torch.from_numpy(v).to(dev) for v in (A, b, c))
+    out = dict(status=torch.empty(3000, dtype=torch.int8, device=dev),
+               objective=torch.empty(3000, dtype=torch.float64, device=dev),
+               x=torch.empty(3000, 32, dtype=torch.float64, device=dev),
+               it1=torch.empty(3000, dtype=torch.int32, device=dev),
+               it2=torch.empty(3000, dtype=torch.int32, device=dev))
+    _native.solve_device(tA, tb, tc, SolverLimits().to_native(), out)
+    torch.cuda.synchronize()
+    compare({k: v.cpu().numpy() for k, v in out.items()}, host, "device-vs-host")
+
+
+def test_full_size_c2_properties():
+    """BASELINE size (1e5 C2 LPs): determinism, chunk invariance and certificate properties."""
+    from paper_1802_08557_b200 import batch_solve_arrays, workloads
+    A, b, c = workloads.afiro_arrays(100_000)
+    r1 = batch_solve_arrays(A, b, c)
+    r2 = batch_solve_arrays(A, b, c)
+    compare(_native_dict(r1), _native_dict(r2), "determinism")
+    half = batch_solve_arrays(A[50_000:], b[50_000:], c[50_000:])
+    compare(_native_dict(half), {k: v[50_000:] for k, v in _native_dict(r1).items()}, "chunk-invariance")
+    opt = r1.status == 0
+    assert 0.85 < opt.mean() < 0.95 and set(np.unique(r1.status)) <= {0, 2}
+    x = r1.x[opt]
+    assert (x >= 0).all()
+    slack = b[opt] - np.einsum("kij,kj->ki", A[opt], x)
+    assert (slack >= -1e-6 * np.maximum(1, np.abs(b[opt]))).all()
+    assert np.allclose(np.einsum("kj,kj->k", c[opt], x), r1.objective[opt], rtol=1e-12, atol=1e-9)
+    # the infeasible recipe rows are exactly the infeasible outcomes
+    assert (r1.status == 2).sum() > 5000
+
+
+def test_c3_sample_against_oracle():
+    """C3 recipe, 2000 fresh LPs (degenerate, unbounded, infeasible, Beale) vs the oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import batch_solve_arrays, workloads
+    A, b, c = workloads.degenerate_arrays(2000, seed=33)
+    res = batch_solve_arrays(A, b, c)
+    compare(_native_dict(res), oracle.solve_batch(A, b, c), "c3-2000")
+    assert set(np.unique(res.status)) == {0, 1, 2}
+
+
+def test_iteration_limit_and_trigger_limits_flow_through():
+    from oracle import oracle
+    from paper_1802_08557_b200 import SolverLimits, batch_solve_arrays, workloads
+    A, b, c = workloads.degenerate_arrays(300, seed=34)
+    for lim in (dict(max_iterations=7), dict(degenerate_pivot_limit=0), dict(degenerate_pivot_limit=3),
+                dict(anti_cycling=False, max_iterations=400)):
+        res = batch_solve_arrays(A, b, c, SolverLimits(**lim))
+        compare(_native_dict(res), oracle.solve_batch(A, b, c, **lim), f"limits {lim}")
