@@ -19,6 +19,7 @@
 #include "../../include/blp.h"
 #include "blp_common.cuh"
 #include "blp_regtile_kernel.cuh"
+#include "blp_warplp_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 
 namespace {
@@ -120,11 +121,28 @@ bool plan_tableau(int m, int n, Plan *p) {
     return true;
 }
 
-// BLP_KERNEL=regtile|smem forces a family (testing / tuning).
+// Warp-per-LP register variant: m <= 32 rows, n + m + 1 <= 64 columns.
+bool plan_warplp(int m, int n, Plan *p) {
+    const int ncols = n + m + 1;
+    if (m > 32) return false;
+    if (ncols <= 32) {
+        p->fn = blp::warplp_kernel<32, 16>; p->name = "warplp_c32"; p->smem = blp::WlpCfg<32>::bytes(m);
+    } else if (ncols <= 64) {
+        p->fn = blp::warplp_kernel<64, 12>; p->name = "warplp_c64"; p->smem = blp::WlpCfg<64>::bytes(m);
+    } else {
+        return false;
+    }
+    p->threads = 32;
+    p->slot = 0;
+    return true;
+}
+
+// BLP_KERNEL=warplp|regtile|smem forces a family (testing / tuning).
 bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
-    const bool allow_rt = !(force && strcmp(force, "smem") == 0);
-    if (allow_rt && plan_regtile(m, n, p)) return true;
+    const bool any = !force || !*force;
+    if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
+    if ((any || strcmp(force, "warplp") == 0 || strcmp(force, "regtile") == 0) && plan_regtile(m, n, p)) return true;
     return plan_tableau(m, n, p);
 }
 
