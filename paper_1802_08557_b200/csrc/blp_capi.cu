@@ -65,11 +65,10 @@ bool plan_regtile(int m, int n, Plan *p) {
     int cpw = env_int("BLP_RT_CPW", rpl == 1 ? 32 : 16);
     struct Inst { int rpl, cpw, maxt; KernelFn fn; const char *name; };
     static const Inst insts[] = {
-        {1, 16, 512, blp::regtile_kernel<1, 16, 512>, "regtile_r1_c16"},
-        {1, 32, 256, blp::regtile_kernel<1, 32, 256>, "regtile_r1_c32"},
-        {1, 64, 128, blp::regtile_kernel<1, 64, 128>, "regtile_r1_c64"},
-        {2, 16, 512, blp::regtile_kernel<2, 16, 512>, "regtile_r2_c16"},
-        {2, 32, 256, blp::regtile_kernel<2, 32, 256>, "regtile_r2_c32"},
+        {1, 16, 128, blp::regtile_kernel<1, 16, 128, 4>, "regtile_r1_c16"},
+        {1, 32, 64, blp::regtile_kernel<1, 32, 64, 8>, "regtile_r1_c32"},
+        {2, 16, 256, blp::regtile_kernel<2, 16, 256, 2>, "regtile_r2_c16"},
+        {2, 32, 128, blp::regtile_kernel<2, 32, 128, 2>, "regtile_r2_c32"},
     };
     for (int attempt = 0; attempt < 2; ++attempt) {
         for (const Inst &I : insts) {
@@ -128,7 +127,13 @@ bool plan_warplp(int m, int n, Plan *p) {
     if (ncols <= 32) {
         p->fn = blp::warplp_kernel<32, 16>; p->name = "warplp_c32"; p->smem = blp::WlpCfg<32>::bytes(m);
     } else if (ncols <= 64) {
-        p->fn = blp::warplp_kernel<64, 12>; p->name = "warplp_c64"; p->smem = blp::WlpCfg<64>::bytes(m);
+        // BLP_WLP_MINB trades registers (= ILP) against resident LPs per SM
+        switch (env_int("BLP_WLP_MINB", 12)) {
+            case 8: p->fn = blp::warplp_kernel<64, 8>; p->name = "warplp_c64_b8"; break;
+            case 10: p->fn = blp::warplp_kernel<64, 10>; p->name = "warplp_c64_b10"; break;
+            default: p->fn = blp::warplp_kernel<64, 12>; p->name = "warplp_c64"; break;
+        }
+        p->smem = blp::WlpCfg<64>::bytes(m);
     } else {
         return false;
     }

@@ -77,6 +77,37 @@ __device__ __forceinline__ bool argmin_before(double a, int ia, double b, int ib
     return a < b || (a == b && ia < ib);
 }
 
+// a / b for tableau entries.  A zero numerator returns a itself (a signed
+// zero, value-equal to IEEE's 0/b); every other quotient is __ddiv_rn.  The
+// zero is replaced by 1 before dividing (not branched around: the compiler
+// if-converts a branch and divides anyway), because __ddiv_rn's range check
+// sends a zero numerator -- in any lane -- to the slow subroutine for the
+// whole warp, and sparse pivot rows are full of zeros.
+// p ? a : b as an opaque PTX selp: the compiler cannot see through it (so it
+// cannot undo the operand substitutions below) and, used as a register-array
+// select, it never turns into a computed index (which would demote the array
+// to local memory).
+__device__ __forceinline__ double selp_f64(double a, double b, bool p) {
+    double r;
+    asm("{ .reg .pred q; setp.ne.u32 q, %3, 0; selp.f64 %0, %1, %2, q; }" : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
+    return r;
+}
+
+__device__ __forceinline__ double div_entry(double a, double b) {
+    const bool z = a == 0.0;
+    const double q = __ddiv_rn(selp_f64(1.0, a, z), b);
+    return z ? a : q;
+}
+
+// choose_leaving's ratio (tableau.py:210-211): rhs / a where a > tol, else
+// SENTINEL.  Operands of the discarded lanes are made harmless for the same
+// fast-path reason as div_entry.
+__device__ __forceinline__ double ratio_entry(double rhs, double a) {
+    const bool ok = a > kTol;
+    const double q = div_entry(selp_f64(rhs, 1.0, ok), selp_f64(a, 1.0, ok));
+    return ok ? q : kSentinel;
+}
+
 // Butterfly reductions: every lane ends with the warp-wide winner.
 __device__ __forceinline__ void warp_argmax(double &v, int &i) {
 #pragma unroll

@@ -48,4 +48,28 @@ __device__ __forceinline__ int warp_index_of(unsigned long long k, unsigned long
 // Keys of the reference thresholds, for comparisons done on keys.
 __device__ __forceinline__ unsigned long long key_of_tol() { return key_max(kTol); }
 
+// a[i] for a warp-uniform runtime index: a uniform branch tree down to
+// groups of 8, then 7 selp's.  Register arrays must only ever be indexed
+// statically -- a computed index (or a switch the compiler turns into one)
+// sends the whole row to local memory.
+template <int LO, int N, int CPW>
+struct RegPicker {
+    static __device__ __forceinline__ double get(const double (&a)[CPW], int i) {
+        if constexpr (N <= 8) {
+            double v = a[LO];
+#pragma unroll
+            for (int k = 1; k < N; ++k) v = selp_f64(a[LO + k], v, i == LO + k);
+            return v;
+        } else {
+            if (i < LO + N / 2) return RegPicker<LO, N / 2, CPW>::get(a, i);
+            return RegPicker<LO + N / 2, N / 2, CPW>::get(a, i);
+        }
+    }
+};
+
+template <int CPW>
+__device__ __forceinline__ double reg_pick(const double (&a)[CPW], int i) {
+    return RegPicker<0, CPW, CPW>::get(a, i);
+}
+
 }  // namespace blp

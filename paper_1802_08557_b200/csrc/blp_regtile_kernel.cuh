@@ -152,15 +152,13 @@ __device__ __forceinline__ void rt_owner_column(const Rt<RPL, CPW> &X, const RtR
     int lr = kNone;
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
-        double av = 0.0;
-#pragma unroll
-        for (int c = 0; c < CPW; ++c) av = (c == ce) ? R.a[s][c] : av;
+        double av = reg_pick<CPW>(R.a[s], ce);
         if (art_e) av = -av;
         const int r = X.lane + 32 * s;
         if (r < X.m) {
             X.fvec[r] = av;
             if (given_l < 0) {
-                const double ratio = av > kTol ? __ddiv_rn(X.rhsv[r], av) : kSentinel;
+                const double ratio = ratio_entry(X.rhsv[r], av);
                 const unsigned long long k = key_min(ratio);
                 if (k < lk) { lk = k; lr = r; }
             }
@@ -169,7 +167,7 @@ __device__ __forceinline__ void rt_owner_column(const Rt<RPL, CPW> &X, const RtR
     double myfm = 0.0;
 #pragma unroll
     for (int t = 0; t < Rt<RPL, CPW>::OPW; ++t)
-        if (X.lane + 32 * t == ce) myfm = art_e ? R.arc[t] : R.rc[t];
+        myfm = selp_f64(art_e ? R.arc[t] : R.rc[t], myfm, X.lane + 32 * t == ce);
     const double fm = __shfl_sync(kFull, myfm, ce & 31);
     int l = given_l;
     unsigned long long kmin = 0;
@@ -211,7 +209,7 @@ __device__ __forceinline__ void rt_update(const Rt<RPL, CPW> &X, RtRegs<RPL, CPW
         const int q = X.lane + 32 * t;
         const int pos = X.warp * CPW + q;
         if (q < CPW && pos < X.ncols) {
-            const double r = __ddiv_rn(rb[q], pe);
+            const double r = div_entry(rb[q], pe);
             rv[q] = r;
             if (pos == 0) {
                 R.rc[t] = __dadd_rn(R.rc[t], __dmul_rn(fm, r));   // tableau.py:242
@@ -396,8 +394,8 @@ __device__ void rt_restore(const Rt<RPL, CPW> &X, RtRegs<RPL, CPW> &R) {
     }
 }
 
-template <int RPL, int CPW, int kMaxThreads>
-__global__ void __launch_bounds__(kMaxThreads)
+template <int RPL, int CPW, int kMaxThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
 regtile_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int nw = blockDim.x >> 5;

@@ -135,7 +135,7 @@ __device__ __forceinline__ void pivot_update(const TabCtx<RPL> &X, int e, int l,
     for (int k = X.lane;; k += 32) {
         const int j = X.warp + X.nw * k;
         if (j >= X.ncols) break;
-        X.rvec[j] = __ddiv_rn(X.T[(size_t)j * ld + l], pe);
+        X.rvec[j] = div_entry(X.T[(size_t)j * ld + l], pe);
     }
     __syncwarp();
     double fr[RPL];
@@ -272,7 +272,7 @@ __device__ PhaseResult run_phase(const TabCtx<RPL> &X, const Limits &lim) {
         for (int i = X.tid; i < m; i += X.nt) {
             const double a = art_e ? -ecol[i] : ecol[i];
             X.fvec[i] = a;
-            const double r = a > kTol ? __ddiv_rn(rcol[i], a) : kSentinel;
+            const double r = ratio_entry(rcol[i], a);
             if (argmin_before(r, i, bv, bi)) { bv = r; bi = i; }
         }
         if (X.tid == 0) X.fvec[m] = art_e ? X.art_rc[e - X.nvc] : ecol[m];

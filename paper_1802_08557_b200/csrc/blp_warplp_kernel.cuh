@@ -13,9 +13,8 @@
 //
 // Numerics follow blp_tableau_kernel.cuh / the reference exactly (separately
 // rounded __dmul_rn/__dsub_rn, IEEE __ddiv_rn, numpy arg-reduction order via
-// the keys of blp_keys.cuh).  The new pivot row is produced as
-// 0 - (-1) * r_j (its lane zeroes its registers and uses factor -1), which is
-// value-equal to numpy's r_j - 0 * r_j for every finite r_j.
+// the keys of blp_keys.cuh).  The new pivot row is r_j itself, reloaded by
+// its lane, value-equal to numpy's r_j - 0 * r_j for every finite r_j.
 #pragma once
 
 #include "blp_common.cuh"
@@ -33,36 +32,6 @@ struct WlpCfg {
     static constexpr size_t STAGE = CBV + 32 * 8;  // m * LDG doubles
     static size_t __host__ __device__ bytes(int m) { return STAGE + (size_t)(m > 0 ? m : 1) * LDG * 8; }
 };
-
-// a[i] for a warp-uniform runtime index: a uniform branch tree down to
-// groups of 8, then 7 selp's.  Register arrays must only ever be indexed
-// statically -- a computed index (or a switch the compiler turns into one)
-// sends the whole row to local memory.
-__device__ __forceinline__ double selp_f64(double a, double b, bool p) {
-    double r;
-    asm("{ .reg .pred q; setp.ne.u32 q, %3, 0; selp.f64 %0, %1, %2, q; }" : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
-    return r;
-}
-
-template <int LO, int N, int CPW>
-struct WlpPicker {
-    static __device__ __forceinline__ double get(const double (&a)[CPW], int i) {
-        if constexpr (N <= 8) {
-            double v = a[LO];
-#pragma unroll
-            for (int k = 1; k < N; ++k) v = selp_f64(a[LO + k], v, i == LO + k);
-            return v;
-        } else {
-            if (i < LO + N / 2) return WlpPicker<LO, N / 2, CPW>::get(a, i);
-            return WlpPicker<LO + N / 2, N / 2, CPW>::get(a, i);
-        }
-    }
-};
-
-template <int CPW>
-__device__ __forceinline__ double wlp_pick(const double (&a)[CPW], int i) {
-    return WlpPicker<0, CPW, CPW>::get(a, i);
-}
 
 enum { kWlpRestore = 0, kWlpPhase1 = 1, kWlpPhase2 = 2 };
 
@@ -109,31 +78,42 @@ __device__ __forceinline__ void wlp_candidates(const WlpDims &D, WlpState<CPW> &
     S.cbl = (int)__reduce_min_sync(kFull, (unsigned)cb);
 }
 
-// pivot (tableau.py:218-244): entering position epos with column values av
-// (this lane's row), leaving row l.  fm = reduced cost of the entering column.
+// Predicated 16-byte shared-memory store / load (one lane of the warp acts;
+// the others keep their registers).  Written as PTX so the row write is 32
+// single-instruction predicated stores instead of a divergent block.
+__device__ __forceinline__ void st_shared_v2_if(bool p, unsigned addr, double x, double y) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.shared.v2.f64 [%1], {%2, %3}; }"
+                 ::"r"((unsigned)p), "r"(addr), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void ld_shared_v2_if(bool p, unsigned addr, double &x, double &y) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.volatile.shared.v2.f64 {%0, %1}, [%3]; }"
+                 : "+d"(x), "+d"(y) : "r"((unsigned)p), "r"(addr) : "memory");
+}
+
+// pivot (tableau.py:218-244): entering column values av (this lane's row),
+// leaving row l, fm = reduced cost of the entering column.  Row l is stored
+// to smem, every lane divides its transposed positions (r = a_lq / pe) and
+// updates its objective slots, every row takes a_ij - f_i * r_j, and the
+// leaving row's lane finally reloads r itself (numpy: r - 0*r == r).
 template <int CPW, int KIND>
 __device__ __forceinline__ void wlp_pivot(const WlpDims &D, WlpState<CPW> &S, unsigned char *smem, int e,
                                           int l, double av, double fm, int oldvar) {
     using C = WlpCfg<CPW>;
     double *rowbuf = reinterpret_cast<double *>(smem + C::ROWBUF);
     double *rvec = reinterpret_cast<double *>(smem + C::RVEC);
+    const unsigned rb = (unsigned)__cvta_generic_to_shared(rowbuf);
+    const unsigned rv = (unsigned)__cvta_generic_to_shared(rvec);
     const double pe = __shfl_sync(kFull, av, l);
-    const double f = D.lane == l ? -1.0 : av;       // lanes >= m hold zeros: av = 0
-    if (D.lane == l) {
+    const bool mine = D.lane == l;
 #pragma unroll
-        for (int c = 0; c < CPW; c += 2) {
-            reinterpret_cast<double2 *>(rowbuf)[c / 2] = make_double2(S.a[c], S.a[c + 1]);
-            S.a[c] = 0.0;
-            S.a[c + 1] = 0.0;
-        }
-        S.basis_r = e;
-    }
+    for (int c = 0; c < CPW; c += 2) st_shared_v2_if(mine, rb + 8u * c, S.a[c], S.a[c + 1]);
+    if (mine) S.basis_r = e;
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < WlpState<CPW>::OPW; ++t) {
         const int pos = D.lane + 32 * t;
         if (pos < D.ncols) {
-            const double r = __ddiv_rn(rowbuf[pos], pe);
+            const double r = div_entry(rowbuf[pos], pe);
             rvec[pos] = r;
             if (pos == 0) {
                 S.rc[t] = __dadd_rn(S.rc[t], __dmul_rn(fm, r));   // tableau.py:242
@@ -156,9 +136,11 @@ __device__ __forceinline__ void wlp_pivot(const WlpDims &D, WlpState<CPW> &S, un
 #pragma unroll
     for (int c = 0; c < CPW; c += 2) {
         const double2 r2 = reinterpret_cast<const double2 *>(rvec)[c / 2];
-        S.a[c] = __dsub_rn(S.a[c], __dmul_rn(f, r2.x));
-        S.a[c + 1] = __dsub_rn(S.a[c + 1], __dmul_rn(f, r2.y));
+        S.a[c] = __dsub_rn(S.a[c], __dmul_rn(av, r2.x));
+        S.a[c + 1] = __dsub_rn(S.a[c + 1], __dmul_rn(av, r2.y));
     }
+#pragma unroll
+    for (int c = 0; c < CPW; c += 2) ld_shared_v2_if(mine, rv + 8u * c, S.a[c], S.a[c + 1]);
 }
 
 // Row of artificial k (the lane whose row got it).
@@ -184,11 +166,12 @@ __device__ __forceinline__ WlpPhase wlp_run_phase(const WlpDims &D, WlpState<CPW
         if (e < 0) return {0, it};
         const bool art_e = e >= D.nvc;
         const int epos = art_e ? 1 + D.n + wlp_row_of_art(S.art_of_r, e - D.nvc) : e + 1;
-        double av = wlp_pick<CPW>(S.a, epos);
+        double av = reg_pick<CPW>(S.a, epos);
         if (art_e) av = -av;
         // choose_leaving (tableau.py:200-215): rhs is register 0
         unsigned long long lk = kKeyEmptyMin;
-        if (D.lane < D.m) lk = key_min(av > kTol ? __ddiv_rn(S.a[0], av) : kSentinel);
+        const double ratio = ratio_entry(S.a[0], av);
+        if (D.lane < D.m) lk = key_min(ratio);
         const unsigned long long kmin = warp_min_key(lk);
         const int l = warp_index_of(lk, kmin, D.lane);
         if (l == kNone || kmin >= kSent) return {1, it};   // unbounded (a NaN ratio keys to 0)
@@ -280,7 +263,7 @@ __device__ __forceinline__ void wlp_restore(const WlpDims &D, WlpState<CPW> &S, 
         bj = __shfl_sync(kFull, bj, row);
         // entries[j] > REDUNDANT_ROW_TOL; a NaN entry compares False in numpy
         if (bj != kNone && bk > kRed && bk != ~0ull) {
-            const double av = wlp_pick<CPW>(S.a, bj + 1);
+            const double av = reg_pick<CPW>(S.a, bj + 1);
             const int oldvar = __shfl_sync(kFull, S.basis_r, row);
             wlp_pivot<CPW, kWlpRestore>(D, S, smem, bj, row, D.lane < D.m ? av : 0.0, 0.0, oldvar);
         }
