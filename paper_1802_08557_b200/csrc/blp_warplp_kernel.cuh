@@ -270,6 +270,18 @@ __device__ __forceinline__ void wlp_restore(const WlpDims &D, WlpState<CPW> &S, 
     }
 }
 
+// L2 prefetch of one LP's A, b, c (128-byte lines spread over the warp).
+__device__ __forceinline__ void prefetch_lp_inputs(const Batch &B, long long lp, int lane) {
+    const size_t mn = (size_t)B.m * B.n;
+    if (!B.shared_Ab) {
+        const char *a = reinterpret_cast<const char *>(B.A + (size_t)lp * mn);
+        for (size_t off = (size_t)lane * 128; off < mn * 8; off += 32 * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a + off));
+        if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.b + (size_t)lp * B.m));
+    }
+    if (lane == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.c + (size_t)lp * B.n));
+}
+
 template <int CPW, int kMinBlocks>
 __global__ void __launch_bounds__(32, kMinBlocks)
 warplp_kernel(Batch B) {
@@ -285,11 +297,17 @@ warplp_kernel(Batch B) {
         for (int q = D.lane; q < CPW; q += 32) { rowbuf[q] = 0.0; rvec[q] = 0.0; }
     }
     WlpState<CPW> S;
+    long long lp = 0;
+    if (D.lane == 0) lp = atomicAdd(B.next_lp, 1);
+    lp = __shfl_sync(kFull, lp, 0);
     for (;;) {
-        long long lp = 0;
-        if (D.lane == 0) lp = atomicAdd(B.next_lp, 1);
-        lp = __shfl_sync(kFull, lp, 0);
         if (lp >= B.count) break;
+        // Claim the next LP now and pull its inputs into L2 while this one is
+        // solved: the queue atomic and the HBM latency leave the critical path.
+        long long nxt = 0;
+        if (D.lane == 0) nxt = atomicAdd(B.next_lp, 1);
+        nxt = __shfl_sync(kFull, nxt, 0);
+        if (nxt < B.count) prefetch_lp_inputs(B, nxt, D.lane);
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;
@@ -304,13 +322,24 @@ warplp_kernel(Batch B) {
         S.art_of_r = neg ? __popc(negmask & ((1u << D.lane) - 1u)) : -1;
         S.basis_r = neg ? nvc + S.art_of_r : n + D.lane;
         if (D.lane < m) stage[D.lane * C::LDG] = __dmul_rn(bi, sgn);
+        // A: lane j loads column j of every row, all loads in flight at once
+#pragma unroll
+        for (int cc = 0; cc < C::OPW; ++cc) {
+            const int j = D.lane + 32 * cc;
+            double v[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) v[r] = (r < m && j < n) ? Ag[(size_t)r * n + j] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const double sr = __shfl_sync(kFull, sgn, r);
+                if (r < m && j < n) {
+                    nonfinite |= !isfinite(v[r]);
+                    stage[r * C::LDG + 1 + j] = __dmul_rn(v[r], sr);
+                }
+            }
+        }
         for (int r = 0; r < m; ++r) {
             const double sr = __shfl_sync(kFull, sgn, r);
-            for (int j = D.lane; j < n; j += 32) {
-                const double a = Ag[(size_t)r * n + j];
-                nonfinite |= !isfinite(a);
-                stage[r * C::LDG + 1 + j] = __dmul_rn(a, sr);
-            }
             for (int q = D.lane; q < m; q += 32) stage[r * C::LDG + 1 + n + q] = q == r ? sr : 0.0;
         }
         for (int j = D.lane; j < n; j += 32) nonfinite |= !isfinite(cg[j]);
@@ -383,6 +412,7 @@ warplp_kernel(Batch B) {
             B.it2[lp] = it2;
         }
         __syncwarp();
+        lp = nxt;
     }
 }
 
