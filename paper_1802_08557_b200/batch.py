@@ -30,6 +30,7 @@ import numpy as np
 
 from . import _native
 from .model import SolveOutcome, StandardFormLP, STATUS_BY_CODE, invalid_message, validate
+from .shard import shard_bounds
 from .simplex import PHASE1_UNBOUNDED_MESSAGE, SolverLimits, outcome_from_arrays
 
 # Column ceiling of the paper's one-block-per-LP Kepler kernel (batch.py:25-29);
@@ -174,7 +175,6 @@ def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared
         if count:
             _native.solve_host(A, b, c, lim, shared_Ab=shared_Ab, device=devices[0], out=out)
         return out
-    per = -(-count // len(devices))
     errors: list[BaseException] = []
 
     def work(dev: int, s: int, e: int) -> None:
@@ -185,8 +185,8 @@ def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared
         except BaseException as err:  # re-raised on the caller's thread
             errors.append(err)
 
-    threads = [threading.Thread(target=work, args=(d, k * per, min(count, (k + 1) * per)))
-               for k, d in enumerate(devices) if k * per < count]
+    threads = [threading.Thread(target=work, args=(d, s, e))
+               for d, (s, e) in zip(devices, shard_bounds(count, len(devices)))]
     for t in threads:
         t.start()
     for t in threads:

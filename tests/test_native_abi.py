@@ -1,0 +1,52 @@
+"""The C ABI library loads and exports every entry point include/blp.h declares.
+
+No compute call is made (no GPU here): only the symbol table and the pure host
+helpers (ABI version, shape support, kernel-variant selection).
+"""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_1802_08557_b200 import _native
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "blp.h"
+
+
+def declared_functions() -> list[str]:
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(blp_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_exported_set():
+    assert declared_functions() == sorted(_native.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_native.LIB_PATH))
+    missing = [name for name in declared_functions() if not hasattr(lib, name)]
+    assert not missing, f"libblp.so lacks {missing}"
+
+
+def test_host_only_entry_points():
+    lib = _native.load()
+    assert lib.blp_abi_version() == 1
+    assert lib.blp_shape_supported(28, 32) == 1
+    assert lib.blp_shape_supported(-1, 3) == 0
+    assert lib.blp_last_error() == b""
+    assert lib.blp_launch_count() >= 0
+
+
+@pytest.mark.parametrize("m,n,family", [(5, 5, "warplp"), (28, 32, "warplp"), (64, 32, "regtile"),
+                                        (100, 100, "smem"), (500, 500, "hbm")])
+def test_kernel_variant_selection(m, n, family):
+    assert _native.kernel_variant(m, n).startswith(family)
+
+
+def test_invalid_arguments_rejected_without_cuda():
+    lib = _native.load()
+    lim = _native.make_limits()
+    rc = lib.blp_solve_batch_host(None, None, None, -1, 2, 2, 0, ctypes.byref(lim), None, None, None, None,
+                                  None, 0)
+    assert rc == -1 and b"invalid" in lib.blp_last_error()
