@@ -152,6 +152,18 @@ def measured_hbm_gbs() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(cfg: str, variant: str, count: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel, from the committed
+    `ncu --set full` capture summary (profiles/traffic.json, scripts/ncu_summary.py), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    for rec in json.loads(p.read_text()):
+        if rec.get("config") == cfg and rec.get("variant") == variant and rec.get("lps_per_launch") == count:
+            return rec.get("dram_bytes_per_launch")
+    return None
+
+
 def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> dict:
     """The oracle port (reference algorithm in C) on all host cores, bounded sample."""
     from oracle import oracle
@@ -309,20 +321,32 @@ def main():
     value = total_lps / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel ----
+    # Algorithmic work per pivot: (m+1)(n+m+1) fp64 cells, each read + written
+    # (16 B) and updated by one multiply + one subtract (2 flops) -- BASELINE.md §2.
     variant = _native.kernel_variant(m, n)
     bpp = bytes_per_pivot(m, n)
-    achieved = pivots * bpp / (step_ms / 1e3) / 1e9
-    if variant.startswith("smem"):
-        peak = _native.probe_smem_gbs(local)
-        bound, peak_src = "smem", "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
-    else:
-        peak, peak_src = measured_hbm_gbs()
-        bound = "hbm"
+    fpp = 2 * (m + 1) * (n + m + 1)
+    secs = step_ms / 1e3
+    achieved_gbs = pivots * bpp / secs / 1e9
+    smem_peak = _native.probe_smem_gbs(local)
     hbm_peak, hbm_src = measured_hbm_gbs()
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_src, "kernel": f"tableau_kernel[{variant}]",
-                "bytes_per_pivot": bpp, "pivots_per_launch": pivots,
-                "hbm_frac": achieved / hbm_peak, "hbm_peak": hbm_peak}
+    fp64_peak = _native.probe_fp64_gflops(local) / 1e3
+    if variant.startswith(("warplp", "regtile")):
+        # tableau in registers: no memory carries it, the FP64 pipe is the ceiling
+        bound, unit, achieved, peak = "fp64", "TFLOP/s", pivots * fpp / secs / 1e12, fp64_peak
+        peak_src = "measured in-run (blp_probe_fp64_gflops: unfused DMUL+DADD chains, all SMs)"
+    elif variant.startswith("smem"):
+        bound, unit, achieved, peak = "smem", "GB/s", achieved_gbs, smem_peak
+        peak_src = "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
+    else:
+        bound, unit, achieved, peak = "hbm", "GB/s", achieved_gbs, hbm_peak
+        peak_src = hbm_src
+    traffic = ncu_traffic(args.config, variant, count)
+    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "kernel": variant,
+                "bytes_per_pivot": bpp, "flops_per_pivot": fpp, "pivots_per_launch": pivots,
+                "tableau_gbs": achieved_gbs, "smem_peak_gbs": smem_peak, "smem_frac": achieved_gbs / smem_peak,
+                "hbm_peak_gbs": hbm_peak, "fp64_peak_tflops": fp64_peak}
 
     # ---- e2e through the public API from pinned host buffers ----
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
@@ -340,6 +364,17 @@ def main():
         r = call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(statistics.median(e2e_t))
+    # PCIe floor for context: one pinned->device copy of this step's inputs
+    tA_h = torch.from_numpy(hA)
+    scratch = torch.empty_like(tA_h, device=dev)
+    torch.cuda.synchronize(dev)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    scratch.copy_(tA_h, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize(dev)
+    h2d_gbs = tA_h.numel() * 8 / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del scratch
     assert np.array_equal(r.status, res["status"]) and np.array_equal(r.x, res["x"]), "e2e result differs"
 
     total_pivots = sum_over_ranks(pivots)
@@ -353,6 +388,7 @@ def main():
         "roofline": roofline,
         "e2e": {"value": total_lps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                "h2d_pinned_gbs": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6,
                 "api": "batch_solve_arrays (blp_solve_batch_host, 3-stream pipelined sub-batches)"},
         "gpu_launches": int(launches),
         "timed_region_ms": region_ms,

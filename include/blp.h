@@ -116,6 +116,11 @@ const char *blp_last_error(void);
  * SMs), the roofline denominator of the smem-resident kernels; < 0 on error. */
 double blp_probe_smem_gbs(int32_t device);
 
+/* Measured unfused FP64 rate of `device` in GFLOP/s (independent DMUL+DADD
+ * chains: one flop each), the roofline denominator of the register-resident
+ * kernels whose rank-1 update is exactly that instruction pair; < 0 on error. */
+double blp_probe_fp64_gflops(int32_t device);
+
 /* BLP_ABI_VERSION of the loaded library. */
 int blp_abi_version(void);
 

@@ -41,7 +41,7 @@ _lib = None
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
 EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
            "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
-           "blp_probe_smem_gbs")
+           "blp_probe_smem_gbs", "blp_probe_fp64_gflops")
 
 
 def load():
@@ -70,6 +70,8 @@ def load():
     lib.blp_last_error.restype = ctypes.c_char_p
     lib.blp_probe_smem_gbs.argtypes = [ctypes.c_int32]
     lib.blp_probe_smem_gbs.restype = ctypes.c_double
+    lib.blp_probe_fp64_gflops.argtypes = [ctypes.c_int32]
+    lib.blp_probe_fp64_gflops.restype = ctypes.c_double
     lib.blp_abi_version.argtypes = []
     lib.blp_abi_version.restype = ctypes.c_int
     _lib = lib
@@ -107,6 +109,15 @@ def probe_smem_gbs(device: int = 0) -> float:
     return v
 
 
+def probe_fp64_gflops(device: int = 0) -> float:
+    """Measured unfused FP64 rate of one GPU (GFLOP/s, DMUL and DADD one flop each)."""
+    _require_gpu()
+    v = float(load().blp_probe_fp64_gflops(int(device)))
+    if v < 0:
+        raise NativeError("fp64 probe failed: " + load().blp_last_error().decode())
+    return v
+
+
 def launch_count() -> int:
     return int(load().blp_launch_count())
 
@@ -119,13 +130,26 @@ def solve_host(A: np.ndarray, b: np.ndarray, c: np.ndarray, limits: Limits, *, s
     count, n = c.shape
     m = b.shape[-1]
     if out is None:
-        out = dict(status=np.empty(count, np.int8), objective=np.empty(count, np.float64),
-                   x=np.empty((count, n), np.float64), it1=np.empty(count, np.int32),
-                   it2=np.empty(count, np.int32))
+        out = alloc_outputs(count, n)
     _check(lib.blp_solve_batch_host(_ptr(A), _ptr(b), _ptr(c), count, m, n, 1 if shared_Ab else 0,
                                     ctypes.byref(limits), _ptr(out["status"]), _ptr(out["objective"]),
                                     _ptr(out["x"]), _ptr(out["it1"]), _ptr(out["it2"]), int(device)))
     return out
+
+
+def alloc_outputs(count: int, n: int) -> dict:
+    """Result arrays in page-locked host memory (torch's caching pinned allocator), so the
+    library's device->host copies stay asynchronous and overlap the next sub-batch."""
+    import torch
+
+    def pinned(shape, dtype):
+        if torch.cuda.is_available():
+            return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+        return np.empty(shape, dtype=torch.empty(0, dtype=dtype).numpy().dtype)
+
+    return dict(status=pinned((count,), torch.int8), objective=pinned((count,), torch.float64),
+                x=pinned((count, n), torch.float64), it1=pinned((count,), torch.int32),
+                it2=pinned((count,), torch.int32))
 
 
 def solve_device(A, b, c, limits: Limits, out: dict, *, shared_Ab: bool = False, stream=None) -> None:

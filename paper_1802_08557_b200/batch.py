@@ -166,9 +166,9 @@ def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared
     """Contiguous LP-index shards, one host thread per device (ctypes releases the GIL)."""
     count, n = c.shape
     if out is None:
-        out = dict(status=np.empty(count, np.int8), objective=np.empty(count, np.float64),
-                   x=np.empty((count, n), np.float64), it1=np.empty(count, np.int32),
-                   it2=np.empty(count, np.int32))
+        out = _native.alloc_outputs(count, n) if count else dict(
+            status=np.empty(0, np.int8), objective=np.empty(0), x=np.empty((0, n)),
+            it1=np.empty(0, np.int32), it2=np.empty(0, np.int32))
     lim = limits.to_native()
     devices = list(devices)[:max(1, count)]
     if len(devices) == 1 or count == 0:

@@ -250,6 +250,22 @@ __global__ void __launch_bounds__(1024) smem_probe_kernel(double *sink, int iter
     if (acc == -1.0) sink[0] = acc;  // keep the loop observable
 }
 
+// FP64 pipe probe: independent DMUL -> DADD chains (unfused, like the tableau
+// update), the roofline denominator of the register-resident kernels.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double *sink, int iters, double s, double t) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __dadd_rn(__dmul_rn(x[k], s), t);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += x[k];
+    if (acc == -1.0) sink[0] = acc;
+}
+
 struct StreamSet {
     std::vector<cudaStream_t> s;
 };
@@ -260,6 +276,31 @@ StreamSet g_streams[64];
 extern "C" {
 
 int blp_abi_version(void) { return BLP_ABI_VERSION; }
+
+double blp_probe_fp64_gflops(int32_t device) {
+    g_last_error.clear();
+    int sms = 0;
+    if (cudaSetDevice(device) != cudaSuccess || device_sms(device, &sms) != BLP_OK) return -1.0;
+    double *sink = nullptr;
+    if (cudaMalloc(&sink, 8) != cudaSuccess) return -1.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = 8 * sms, threads = 256, iters = 8192;
+    fp64_probe_kernel<<<grid, threads>>>(sink, 64, 0.999999, 1e-7);  // warm-up
+    cudaEventRecord(e0);
+    fp64_probe_kernel<<<grid, threads>>>(sink, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    float ms = 0.f;
+    const bool ok = cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (!ok || ms <= 0.f) return -1.0;
+    const double flops = 2.0 * 8.0 * (double)iters * grid * threads;  // one DMUL + one DADD per step
+    return flops / (ms * 1e-3) / 1e9;
+}
 
 double blp_probe_smem_gbs(int32_t device) {
     g_last_error.clear();
