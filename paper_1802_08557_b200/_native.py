@@ -137,6 +137,16 @@ def solve_host(A: np.ndarray, b: np.ndarray, c: np.ndarray, limits: Limits, *, s
     return out
 
 
+def alloc_host(shape, dtype=np.float64) -> np.ndarray:
+    """Page-locked host array when a GPU is visible (torch's caching pinned allocator), else plain."""
+    import torch
+    if torch.cuda.is_available():
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32,
+               np.dtype(np.int8): torch.int8}[np.dtype(dtype)]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+    return np.empty(shape, dtype)
+
+
 def alloc_outputs(count: int, n: int) -> dict:
     """Result arrays in page-locked host memory (torch's caching pinned allocator), so the
     library's device->host copies stay asynchronous and overlap the next sub-batch."""

@@ -279,9 +279,10 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
     # non-finite entries are flagged by the kernel (BLP_STATUS_INVALID).
     bad_shape = _first_bad_shape(lps, m, n)
     limit = bad_shape if bad_shape >= 0 else len(lps)
-    A = np.empty((limit, m, n), np.float64)
-    b = np.empty((limit, m), np.float64)
-    c = np.empty((limit, n), np.float64)
+    # packed straight into page-locked buffers: the library's H2D copies run at full PCIe rate
+    A = _native.alloc_host((limit, m, n))
+    b = _native.alloc_host((limit, m))
+    c = _native.alloc_host((limit, n))
     for k in range(limit):
         lp = lps[k]
         A[k] = lp.A

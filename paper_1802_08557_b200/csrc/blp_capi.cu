@@ -369,7 +369,7 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
     if (count == 0) return BLP_OK;
     if (device < 0 || device >= 64) return fail(BLP_ERR_INVALID, "device index out of range");
     BLP_CUDA_TRY(cudaSetDevice(device));
-    constexpr int kStreams = 3;
+    constexpr int kStreams = 4;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         auto &ss = g_streams[device].s;
@@ -380,7 +380,11 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
     }
     const auto &ss = g_streams[device].s;
     // Sub-batches: at least 8192 LPs each, at most 8 of them.
-    const long long chunk = std::max<long long>(8192, (count + 7) / 8);
+    // Sub-batches: BLP_HOST_CHUNKS of them (default 32), at least 2048 LPs each
+    // (measured on C2: 4 -> 17.0 ms, 8 -> 15.5, 16 -> 15.2, 32 -> 14.9, 64 -> 15.2 per 1e5,
+    // against a 13.8 ms pinned-H2D floor).
+    const int nchunks = std::max(1, env_int("BLP_HOST_CHUNKS", 32));
+    const long long chunk = std::max<long long>(2048, (count + nchunks - 1) / nchunks);
     const size_t szA = (size_t)m * n, szb = (size_t)m;
 
     // Shared polytope (support-function mode): one H2D, every stream waits on it.
