@@ -27,6 +27,7 @@
 #pragma once
 
 #include "blp_common.cuh"
+#include "blp_keys.cuh"
 
 namespace blp {
 
@@ -81,9 +82,9 @@ struct TabCtx {
     double *rvec;     // pivot row / pe, written and read by the owning warp only
     double *art_rc;   // phase-1 reduced costs of the artificial columns
     double *cbv;      // basic costs during price-out
-    double *cval;     // per-warp entering candidates (value, index, Bland index)
+    unsigned long long *ckey;  // per-warp entering candidates (key, index, Bland index)
     int *cidx, *cbl;
-    double *lval;     // per-warp leaving candidates (ratio, row)
+    unsigned long long *lkey;  // per-warp leaving candidates (ratio key, row)
     int *lrow;
     int *basis, *art_row, *art_of;
     long long *misc;
@@ -92,50 +93,63 @@ struct TabCtx {
 };
 
 // ---------------------------------------------------------------------------
-// Entering-variable selection from the per-warp partials (after a barrier).
-// choose_entering (tableau.py:175-186) or choose_entering_bland (:189-197).
+// Arg-reductions on numpy-order keys (blp_keys.cuh): per-warp partials are
+// (key, index) pairs in smem; every warp reduces them after a barrier.
+
+// Per-thread running best for the entering choice: Dantzig (max key, lowest
+// index) and Bland (lowest index with rc > tol).
+struct EnterBest {
+    unsigned long long k = kKeyEmptyMax;
+    int i = kNone, bl = kNone;
+    __device__ __forceinline__ void add(double v, int j) {
+        const unsigned long long kv = key_max(v);
+        if (kv > k || (kv == k && j < i)) { k = kv; i = j; }
+        if (v > kTol && j < bl) bl = j;
+    }
+};
+
+template <int RPL>
+__device__ __forceinline__ void publish_candidates(const TabCtx<RPL> &X, const EnterBest &b) {
+    const unsigned long long kw = warp_max_key(b.k);
+    const int iw = warp_index_of(b.k, kw, b.i);
+    const int bw = warp_min_int(b.bl);
+    if (X.lane == 0) { X.ckey[X.warp] = kw; X.cidx[X.warp] = iw; X.cbl[X.warp] = bw; }
+}
+
+// choose_entering (tableau.py:175-186) / choose_entering_bland (:189-197).
 template <int RPL>
 __device__ __forceinline__ int select_entering(const TabCtx<RPL> &X, bool use_bland) {
-    double v = -__longlong_as_double(0x7ff0000000000000LL);  // -inf
-    int i = kNone, bl = kNone;
-    if (X.lane < X.nw) { v = X.cval[X.lane]; i = X.cidx[X.lane]; bl = X.cbl[X.lane]; }
-    warp_argmax(v, i);
-    bl = warp_min_int(bl);
+    unsigned long long k = kKeyEmptyMax;
+    int i = kNone, b = kNone;
+    if (X.lane < X.nw) { k = X.ckey[X.lane]; i = X.cidx[X.lane]; b = X.cbl[X.lane]; }
+    const unsigned long long kw = warp_max_key(k);
+    const int e = warp_index_of(k, kw, i);
+    const int bl = warp_min_int(b);
     if (use_bland) return bl == kNone ? -1 : bl;
-    if (i == kNone) return -1;          // no selectable non-basic column
-    if (v <= kTol) return -1;           // optimal (NaN is not <= tol: numpy returns it)
-    return i;
-}
-
-template <int RPL>
-__device__ __forceinline__ void publish_candidates(const TabCtx<RPL> &X, double cv, int ci, int cb) {
-    warp_argmax(cv, ci);
-    cb = warp_min_int(cb);
-    if (X.lane == 0) { X.cval[X.warp] = cv; X.cidx[X.warp] = ci; X.cbl[X.warp] = cb; }
-}
-
-__device__ __forceinline__ void consider(double v, int j, double &cv, int &ci, int &cb) {
-    if (argmax_before(v, j, cv, ci)) { cv = v; ci = j; }
-    if (v > kTol && j < cb) cb = j;
+    if (e == kNone || kw <= key_max(kTol)) return -1;   // NaN keys sort above tol, as numpy
+    return e;
 }
 
 // ---------------------------------------------------------------------------
 // Rank-1 pivot update on the columns this warp owns (pivot, tableau.py:218-244).
 // Preconditions: fvec holds column e (rows 0..m) as it was before the pivot;
 // every thread knows (e, l, pe, fm = reduced cost of e, oldvar = basis[l]).
-// Computes r_j = a_lj / pe for the warp's columns, then
-//   a_ij <- a_ij - f_i * r_j   (row l: r_j - 0 * r_j, as numpy does after the
-//   in-place row division; objective cell: obj_before + rc_e * r_rhs).
-// Phase 1/2: also produces the next entering candidates of the owned columns.
+//   1. lane k divides the pivot-row entry of the warp's k-th column;
+//   2. a_ij <- a_ij - f_i * r_j on every owned cell (f_l = 0 leaves row l);
+//   3. row l's lane writes r_j into row l (numpy: r_j - 0*r_j == r_j);
+//   4. lane k finishes column k's objective cell: the reduced cost it now holds
+//      is tested as the next entering candidate (plus, in phase 1, the paired
+//      artificial's), the rhs column gets obj_before + rc_e * r_rhs (tableau.py:242).
 template <int RPL, int KIND>
 __device__ __forceinline__ void pivot_update(const TabCtx<RPL> &X, int e, int l, double pe,
                                              double fm, int oldvar) {
     const int m = X.m, ld = X.ld;
-    // pivot row division, one column per lane of the owning warp
+    double obj_before = 0.0;
     for (int k = X.lane;; k += 32) {
         const int j = X.warp + X.nw * k;
         if (j >= X.ncols) break;
         X.rvec[j] = div_entry(X.T[(size_t)j * ld + l], pe);
+        if (j == X.rhs) obj_before = X.T[(size_t)j * ld + m];
     }
     __syncwarp();
     double fr[RPL];
@@ -144,42 +158,42 @@ __device__ __forceinline__ void pivot_update(const TabCtx<RPL> &X, int e, int l,
         const int i = X.lane + 32 * s;
         fr[s] = (i <= m && i != l) ? X.fvec[i] : 0.0;
     }
-    double cv = -__longlong_as_double(0x7ff0000000000000LL);
-    int ci = kNone, cb = kNone;
     for (int j = X.warp; j < X.ncols; j += X.nw) {
         const double rj = X.rvec[j];
         double *col = X.T + (size_t)j * ld;
 #pragma unroll
         for (int s = 0; s < RPL; ++s) {
             const int i = X.lane + 32 * s;
-            if (i <= m) {
-                const double a = (i == l) ? rj : col[i];
-                double v = __dsub_rn(a, __dmul_rn(fr[s], rj));
-                if (i == m) {
-                    if (j == X.rhs) {
-                        v = __dadd_rn(a, __dmul_rn(fm, rj));   // tableau.py:242
-                    } else if (KIND != kRestore) {
-                        const bool basic = (j == e) || (j != oldvar && X.isb[j]);
-                        if (!basic) consider(v, j, cv, ci, cb);
-                        if (KIND == kPhase1 && j >= X.n) {
-                            const int k = X.art_of[j - X.n];
-                            if (k >= 0) {
-                                // artificial k: column = -(slack column of its row),
-                                // so its pivot-row entry is -r_j exactly
-                                const double nr = __dsub_rn(X.art_rc[k], __dmul_rn(fm, -rj));
-                                X.art_rc[k] = nr;
-                                const int ja = X.nvc + k;
-                                const bool abasic = (ja == e) || (ja != oldvar && X.isb[ja]);
-                                if (!abasic) consider(nr, ja, cv, ci, cb);
-                            }
-                        }
-                    }
+            if (i <= m) col[i] = __dsub_rn(col[i], __dmul_rn(fr[s], rj));
+        }
+    }
+    if (X.lane == (l & 31)) {
+        for (int j = X.warp; j < X.ncols; j += X.nw) X.T[(size_t)j * ld + l] = X.rvec[j];
+    }
+    __syncwarp();
+    EnterBest best;
+    for (int k = X.lane;; k += 32) {
+        const int j = X.warp + X.nw * k;
+        if (j >= X.ncols) break;
+        const double rj = X.rvec[j];
+        if (j == X.rhs) {
+            X.T[(size_t)j * ld + m] = __dadd_rn(obj_before, __dmul_rn(fm, rj));
+        } else if (KIND != kRestore) {
+            const bool basic = (j == e) || (j != oldvar && X.isb[j]);
+            if (!basic) best.add(X.T[(size_t)j * ld + m], j);
+            if (KIND == kPhase1 && j >= X.n) {
+                const int k2 = X.art_of[j - X.n];
+                if (k2 >= 0) {
+                    // artificial k2 = -(slack column of its row): pivot-row entry -r_j exactly
+                    const double nr = __dsub_rn(X.art_rc[k2], __dmul_rn(fm, -rj));
+                    X.art_rc[k2] = nr;
+                    const int ja = X.nvc + k2;
+                    if (!((ja == e) || (ja != oldvar && X.isb[ja]))) best.add(nr, ja);
                 }
-                col[i] = v;
             }
         }
     }
-    if (KIND != kRestore) publish_candidates(X, cv, ci, cb);
+    if (KIND != kRestore) publish_candidates(X, best);
 }
 
 // ---------------------------------------------------------------------------
@@ -199,8 +213,7 @@ __device__ void price_out(const TabCtx<RPL> &X, const double *cg) {
         X.cbv[i] = cb;
     }
     __syncthreads();
-    double cv = -__longlong_as_double(0x7ff0000000000000LL);
-    int ci = kNone, cbl = kNone;
+    EnterBest best;
     const int nart = PHASE == 1 ? X.n_art : 0;
     const int total = X.nvc + nart + 1;
     for (int q = X.tid; q < total; q += X.nt) {
@@ -212,7 +225,7 @@ __device__ void price_out(const TabCtx<RPL> &X, const double *cg) {
                 if (cb != 0.0) rc = __dsub_rn(rc, __dmul_rn(cb, col[r]));
             }
             X.T[(size_t)q * ld + m] = rc;
-            if (!X.isb[q]) consider(rc, q, cv, ci, cbl);
+            if (!X.isb[q]) best.add(rc, q);
         } else if (q < X.nvc + nart) {
             const int k = q - X.nvc;
             const double *scol = X.T + (size_t)(X.n + X.art_row[k]) * ld;
@@ -222,7 +235,7 @@ __device__ void price_out(const TabCtx<RPL> &X, const double *cg) {
                 if (cb != 0.0) rc = __dsub_rn(rc, __dmul_rn(cb, -scol[r]));
             }
             X.art_rc[k] = rc;
-            if (!X.isb[q]) consider(rc, q, cv, ci, cbl);
+            if (!X.isb[q]) best.add(rc, q);
         } else {
             const double *col = X.T + (size_t)X.rhs * ld;
             double obj = 0.0;
@@ -233,7 +246,7 @@ __device__ void price_out(const TabCtx<RPL> &X, const double *cg) {
             X.T[(size_t)X.rhs * ld + m] = obj;
         }
     }
-    publish_candidates(X, cv, ci, cbl);
+    publish_candidates(X, best);
     __syncthreads();
 }
 
@@ -241,11 +254,10 @@ __device__ void price_out(const TabCtx<RPL> &X, const double *cg) {
 // reference runs phase 2 on c without a price-out, simplex.py:168,180).
 template <int RPL>
 __device__ void initial_candidates(const TabCtx<RPL> &X) {
-    double cv = -__longlong_as_double(0x7ff0000000000000LL);
-    int ci = kNone, cbl = kNone;
+    EnterBest best;
     for (int j = X.tid; j < X.nvc; j += X.nt)
-        if (!X.isb[j]) consider(X.T[(size_t)j * X.ld + X.m], j, cv, ci, cbl);
-    publish_candidates(X, cv, ci, cbl);
+        if (!X.isb[j]) best.add(X.T[(size_t)j * X.ld + X.m], j);
+    publish_candidates(X, best);
     __syncthreads();
 }
 
@@ -257,6 +269,7 @@ __device__ PhaseResult run_phase(const TabCtx<RPL> &X, const Limits &lim) {
     const int m = X.m, ld = X.ld;
     const int max_iter = lim.max_iterations > 0 ? lim.max_iterations : 50 * (m + X.n);
     const int trigger = lim.degenerate_limit >= 0 ? lim.degenerate_limit : (m > 1 ? m : 1);
+    const unsigned long long kSent = key_max(kSentinel), kDeg = key_max(kDegenerateTol);
     int degenerate_run = 0;
     bool use_bland = false;
     for (int it = 0;; ++it) {
@@ -267,27 +280,31 @@ __device__ PhaseResult run_phase(const TabCtx<RPL> &X, const Limits &lim) {
         const bool art_e = e >= X.nvc;
         const double *ecol = X.T + (size_t)(art_e ? X.n + X.art_row[e - X.nvc] : e) * ld;
         const double *rcol = X.T + (size_t)X.rhs * ld;
-        double bv = __longlong_as_double(0x7ff0000000000000LL);
-        int bi = kNone;
+        unsigned long long lk = kKeyEmptyMin;
+        int li = kNone;
         for (int i = X.tid; i < m; i += X.nt) {
             const double a = art_e ? -ecol[i] : ecol[i];
             X.fvec[i] = a;
-            const double r = ratio_entry(rcol[i], a);
-            if (argmin_before(r, i, bv, bi)) { bv = r; bi = i; }
+            const unsigned long long k = key_min(ratio_entry(rcol[i], a));
+            if (k < lk) { lk = k; li = i; }     // rows ascend per thread
         }
         if (X.tid == 0) X.fvec[m] = art_e ? X.art_rc[e - X.nvc] : ecol[m];
-        warp_argmin(bv, bi);
-        if (X.lane == 0) { X.lval[X.warp] = bv; X.lrow[X.warp] = bi; }
+        {
+            const unsigned long long kw = warp_min_key(lk);
+            const int iw = warp_index_of(lk, kw, li);
+            if (X.lane == 0) { X.lkey[X.warp] = kw; X.lrow[X.warp] = iw; }
+        }
         __syncthreads();  // B2
-        double v = __longlong_as_double(0x7ff0000000000000LL);
-        int l = kNone;
-        if (X.lane < X.nw) { v = X.lval[X.lane]; l = X.lrow[X.lane]; }
-        warp_argmin(v, l);
-        if (l == kNone || v >= kSentinel) return {1, it};
+        unsigned long long k = kKeyEmptyMin;
+        int i = kNone;
+        if (X.lane < X.nw) { k = X.lkey[X.lane]; i = X.lrow[X.lane]; }
+        const unsigned long long kmin = warp_min_key(k);
+        const int l = warp_index_of(k, kmin, i);
+        if (l == kNone || kmin >= kSent) return {1, it};   // a NaN ratio keys to 0
         const int oldvar = X.basis[l];
         const double pe = X.fvec[l];
         const double fm = X.fvec[m];
-        if (v <= kDegenerateTol) {            // simplex.py:84-90
+        if (kmin != 0ull && kmin <= kDeg) {                 // simplex.py:84-90
             ++degenerate_run;
             if (lim.anti_cycling && degenerate_run >= trigger) use_bland = true;
         } else {
@@ -304,23 +321,29 @@ __device__ PhaseResult run_phase(const TabCtx<RPL> &X, const Limits &lim) {
 template <int RPL>
 __device__ void restore_basis(const TabCtx<RPL> &X) {
     const int m = X.m, ld = X.ld;
+    const unsigned long long kRed = key_max(kRedundantTol);
     __syncthreads();
     for (int row = 0; row < m; ++row) {
         if (X.basis[row] < X.nvc) continue;   // uniform: basis is stable here
-        double bv = -__longlong_as_double(0x7ff0000000000000LL);
+        unsigned long long bk = kKeyEmptyMax;
         int bj = kNone;
         for (int j = X.tid; j < X.nvc; j += X.nt) {
-            const double v = fabs(X.T[(size_t)j * ld + row]);
-            if (argmax_before(v, j, bv, bj)) { bv = v; bj = j; }
+            const unsigned long long k = key_max(fabs(X.T[(size_t)j * ld + row]));
+            if (k > bk) { bk = k; bj = j; }     // columns ascend per thread
         }
-        warp_argmax(bv, bj);
-        if (X.lane == 0) { X.cval[X.warp] = bv; X.cidx[X.warp] = bj; }
+        {
+            const unsigned long long kw = warp_max_key(bk);
+            const int jw = warp_index_of(bk, kw, bj);
+            if (X.lane == 0) { X.ckey[X.warp] = kw; X.cidx[X.warp] = jw; }
+        }
         __syncthreads();
-        double v = -__longlong_as_double(0x7ff0000000000000LL);
-        int j = kNone;
-        if (X.lane < X.nw) { v = X.cval[X.lane]; j = X.cidx[X.lane]; }
-        warp_argmax(v, j);
-        if (j != kNone && v > kRedundantTol) {
+        unsigned long long k = kKeyEmptyMax;
+        int jj = kNone;
+        if (X.lane < X.nw) { k = X.ckey[X.lane]; jj = X.cidx[X.lane]; }
+        const unsigned long long kbest = warp_max_key(k);
+        const int j = warp_index_of(k, kbest, jj);
+        // entries[j] > REDUNDANT_ROW_TOL; a NaN entry compares False in numpy
+        if (j != kNone && kbest > kRed && kbest != ~0ull) {
             for (int i = X.tid; i <= m; i += X.nt) X.fvec[i] = X.T[(size_t)j * ld + i];
             __syncthreads();
             const int oldvar = X.basis[row];
@@ -350,8 +373,8 @@ tableau_kernel(Batch B) {
     X.rvec = reinterpret_cast<double *>(smem + L.off_r);
     X.art_rc = reinterpret_cast<double *>(smem + L.off_artrc);
     X.cbv = reinterpret_cast<double *>(smem + L.off_cbv);
-    X.cval = reinterpret_cast<double *>(smem + L.off_cval);
-    X.lval = reinterpret_cast<double *>(smem + L.off_lval);
+    X.ckey = reinterpret_cast<unsigned long long *>(smem + L.off_cval);
+    X.lkey = reinterpret_cast<unsigned long long *>(smem + L.off_lval);
     X.cidx = reinterpret_cast<int *>(smem + L.off_cidx);
     X.cbl = reinterpret_cast<int *>(smem + L.off_cbl);
     X.lrow = reinterpret_cast<int *>(smem + L.off_lrow);
