@@ -110,9 +110,9 @@ bool plan_tableau(int m, int n, Plan *p) {
     const int ncols = n + m + 1;
     int ctas = smem_tab ? (int)std::max<size_t>(1, (228 * 1024) / (Ls.bytes + 1024)) : 2;
     ctas = std::min(ctas, 16);
-    int warps = std::max(2, 32 / ctas);
+    int warps = std::max(2, std::min(16, 32 / ctas));   // C3 (1 CTA/SM): 16 beats 8 and 32
     warps = std::min(warps, std::max(1, (ncols + 1) / 2));
-    warps = std::min(warps, maxt / 32);
+    warps = std::min(env_int("BLP_TAB_WARPS", warps), maxt / 32);
     p->threads = std::max(1, warps) * 32;
     const blp::TabLayout L = blp::make_tab_layout(m, n, p->threads / 32, smem_tab);
     p->smem = L.bytes;

@@ -44,7 +44,7 @@ __host__ __device__ inline size_t tl_align(size_t x, size_t a) { return (x + a -
 
 __host__ __device__ inline TabLayout make_tab_layout(int m, int n, int nwarps, bool smem_tab) {
     TabLayout L;
-    L.ld = (m + 2) & ~1;
+    L.ld = (m + 3) & ~1;   // >= m+2: row m+1 is a spare row (see pivot_update)
     L.ncols = n + m + 1;
     const int mm = m > 0 ? m : 1;
     size_t o = 0;
@@ -158,13 +158,21 @@ __device__ __forceinline__ void pivot_update(const TabCtx<RPL> &X, int e, int l,
         const int i = X.lane + 32 * s;
         fr[s] = (i <= m && i != l) ? X.fvec[i] : 0.0;
     }
-    for (int j = X.warp; j < X.ncols; j += X.nw) {
-        const double rj = X.rvec[j];
-        double *col = X.T + (size_t)j * ld;
+    // Lanes past the last row all address the spare row m+1 (ld >= m+2) with
+    // factor 0: a benign same-value store, and no per-slot branch in the loop.
+    {
+        int roff[RPL];
 #pragma unroll
-        for (int s = 0; s < RPL; ++s) {
-            const int i = X.lane + 32 * s;
-            if (i <= m) col[i] = __dsub_rn(col[i], __dmul_rn(fr[s], rj));
+        for (int s = 0; s < RPL; ++s) roff[s] = min(X.lane + 32 * s, m + 1);
+        double *col = X.T + (size_t)X.warp * ld;
+        const size_t cstride = (size_t)ld * X.nw;
+        for (int j = X.warp; j < X.ncols; j += X.nw, col += cstride) {
+            const double rj = X.rvec[j];
+            double a[RPL];
+#pragma unroll
+            for (int s = 0; s < RPL; ++s) a[s] = col[roff[s]];
+#pragma unroll
+            for (int s = 0; s < RPL; ++s) col[roff[s]] = __dsub_rn(a[s], __dmul_rn(fr[s], rj));
         }
     }
     if (X.lane == (l & 31)) {
