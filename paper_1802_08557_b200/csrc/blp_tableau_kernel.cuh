@@ -136,7 +136,7 @@ __device__ __forceinline__ int select_entering(const TabCtx<RPL> &X, bool use_bl
 // every thread knows (e, l, pe, fm = reduced cost of e, oldvar = basis[l]).
 //   1. lane k divides the pivot-row entry of the warp's k-th column;
 //   2. a_ij <- a_ij - f_i * r_j on every owned cell (f_l = 0 leaves row l);
-//   3. row l's lane writes r_j into row l (numpy: r_j - 0*r_j == r_j);
+//   3. lane k writes r_j into row l of its column (numpy: r_j - 0*r_j == r_j);
 //   4. lane k finishes column k's objective cell: the reduced cost it now holds
 //      is tested as the next entering candidate (plus, in phase 1, the paired
 //      artificial's), the rhs column gets obj_before + rc_e * r_rhs (tableau.py:242).
@@ -175,8 +175,12 @@ __device__ __forceinline__ void pivot_update(const TabCtx<RPL> &X, int e, int l,
             for (int s = 0; s < RPL; ++s) col[roff[s]] = __dsub_rn(a[s], __dmul_rn(fr[s], rj));
         }
     }
-    if (X.lane == (l & 31)) {
-        for (int j = X.warp; j < X.ncols; j += X.nw) X.T[(size_t)j * ld + l] = X.rvec[j];
+    __syncwarp();
+    // row l <- r, one column per lane (after the update wrote row l unchanged)
+    for (int k = X.lane;; k += 32) {
+        const int j = X.warp + X.nw * k;
+        if (j >= X.ncols) break;
+        X.T[(size_t)j * ld + l] = X.rvec[j];
     }
     __syncwarp();
     EnterBest best;
