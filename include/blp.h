@@ -100,6 +100,22 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c,
                          int32_t *iters1, int32_t *iters2,
                          int32_t device);
 
+/*
+ * Batched hyper-rectangle LPs (the paper's Eq. 7 kernel; reference
+ * boxlp.py:44-83 solve_box / solve_box_batch): maximise direction.x over
+ * lower <= x <= upper for `count` boxes of dimension n, row-major [count][n].
+ * value [count] (NaN if invalid), point [count][n] (zeros if invalid),
+ * status [count]: 0 valid; -1 a non-finite bound ("box bounds must be
+ * finite"); k+1 lower[k] > upper[k] at the first such k (boxlp.py:57-61).
+ * _device: device pointers, async on cuda_stream; _host: host buffers, synchronous.
+ */
+int blp_box_solve_device(const double *lower, const double *upper, const double *direction,
+                         int64_t count, int32_t n, double *value, double *point, int32_t *status,
+                         void *cuda_stream);
+int blp_box_solve_host(const double *lower, const double *upper, const double *direction,
+                       int64_t count, int32_t n, double *value, double *point, int32_t *status,
+                       int32_t device);
+
 /* Largest (m, n) the library accepts: 1 if supported, 0 otherwise. */
 int blp_shape_supported(int32_t m, int32_t n);
 

@@ -93,3 +93,33 @@ def host_cores() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def box_solve(lower, upper, direction) -> dict:
+    """Hyper-rectangle LPs, restating boxlp.py:44-61 row by row (numpy, CPU): value (left-to-right
+    sum; NaN if invalid), point (zeros if invalid), status (0 ok, -1 non-finite bound, k+1 first
+    lower > upper, 1 when the only fault is lower+upper overflowing)."""
+    lower = np.asarray(lower, np.float64)
+    upper = np.asarray(upper, np.float64)
+    direction = np.asarray(direction, np.float64)
+    count, n = direction.shape
+    value = np.full(count, np.nan)
+    point = np.zeros((count, n))
+    status = np.zeros(count, np.int32)
+    for k in range(count):
+        lo, hi, d = lower[k], upper[k], direction[k]
+        with np.errstate(over="ignore", invalid="ignore"):
+            ok = bool(((lo <= hi) & np.isfinite(lo + hi)).all())       # boxlp.py:51
+        if not ok:
+            if not (np.isfinite(lo).all() and np.isfinite(hi).all()):   # boxlp.py:58-59
+                status[k] = -1
+            else:
+                status[k] = 1 + int(np.argmax(lo > hi))                  # boxlp.py:60
+            continue
+        p = np.where(d < 0, lo, hi)                                      # boxlp.py:53
+        s = 0.0
+        for j in range(n):
+            s = s + d[j] * p[j]
+        point[k] = p
+        value[k] = s
+    return dict(value=value, point=point, status=status)

@@ -7,7 +7,9 @@ their types, with the simplex itself running as hand-written sm_100a CUDA in
 libblp.so (C ABI: include/blp.h).  There is no CPU fallback.
 
 Packed fast paths: ``batch_solve_arrays`` (A [B,m,n], b [B,m], c [B,n]) and
-``support_batch`` (one polytope, many objective directions).
+``support_batch`` (one polytope, many objective directions).  The paper's
+second kernel, batched hyper-rectangle LPs (Eq. 7), is ``solve_box_batch`` /
+``box_batch_arrays`` (reference boxlp.py).
 """
 from .batch import (
     REFERENCE_GPU_BLOCK_COLS,
@@ -23,12 +25,14 @@ from .batch import (
     plan_chunks,
     support_batch,
 )
+from .boxlp import BoxArrays, BoxLP, BoxSolution, InvalidBox, box_batch_arrays, solve_box, solve_box_batch
 from .model import SolveOutcome, StandardFormLP, Status, standard_form, validate
 from .simplex import SolverLimits, solve
 from .workloads import gen_random_lps
 from ._native import NativeError, NativeUnavailable
 
 __all__ = [
+    "BoxArrays", "BoxLP", "BoxSolution", "InvalidBox", "box_batch_arrays", "solve_box", "solve_box_batch",
     "BatchArrays", "BatchConfig", "BatchReport", "BatchTooLarge", "ChunkPlan", "HeterogeneousBatch",
     "NativeError", "NativeUnavailable", "REFERENCE_GPU_BLOCK_COLS", "SolveOutcome", "SolverLimits",
     "StandardFormLP", "Status", "batch_solve", "batch_solve_arrays", "gen_random_lps", "lp_memory_bytes",

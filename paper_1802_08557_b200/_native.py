@@ -41,7 +41,7 @@ _lib = None
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
 EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
            "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
-           "blp_probe_smem_gbs", "blp_probe_fp64_gflops")
+           "blp_probe_smem_gbs", "blp_probe_fp64_gflops", "blp_box_solve_device", "blp_box_solve_host")
 
 
 def load():
@@ -74,8 +74,24 @@ def load():
     lib.blp_probe_fp64_gflops.restype = ctypes.c_double
     lib.blp_abi_version.argtypes = []
     lib.blp_abi_version.restype = ctypes.c_int
+    box = [P, P, P, ctypes.c_int64, ctypes.c_int32, P, P, P]
+    lib.blp_box_solve_device.argtypes = box + [P]
+    lib.blp_box_solve_device.restype = ctypes.c_int
+    lib.blp_box_solve_host.argtypes = box + [ctypes.c_int32]
+    lib.blp_box_solve_host.restype = ctypes.c_int
     _lib = lib
     return lib
+
+
+def box_solve_host(lower: np.ndarray, upper: np.ndarray, direction: np.ndarray, device: int = 0) -> dict:
+    """Packed hyper-rectangle LPs [count, n] -> value, point, status (blp_box_solve_host)."""
+    lib = load()
+    _require_gpu()
+    count, n = direction.shape
+    out = dict(value=alloc_host((count,)), point=alloc_host((count, n)), status=alloc_host((count,), np.int32))
+    _check(lib.blp_box_solve_host(_ptr(lower), _ptr(upper), _ptr(direction), count, n, _ptr(out["value"]),
+                                  _ptr(out["point"]), _ptr(out["status"]), int(device)))
+    return out
 
 
 def _check(rc: int) -> None:

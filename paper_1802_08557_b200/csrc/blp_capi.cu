@@ -21,6 +21,7 @@
 #include "blp_regtile_kernel.cuh"
 #include "blp_warplp_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
+#include "blp_box_kernel.cuh"
 
 namespace {
 
@@ -452,6 +453,60 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
             rc = fail(BLP_ERR_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(e));
     }
     if (shared_ready) cudaEventDestroy(shared_ready);
+    return rc;
+}
+
+int blp_box_solve_device(const double *lower, const double *upper, const double *direction, int64_t count,
+                         int32_t n, double *value, double *point, int32_t *status, void *cuda_stream) {
+    g_last_error.clear();
+    if (count < 0 || n < 0 || (count > 0 && (!value || !status || (n > 0 && (!lower || !upper || !direction || !point)))))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    int dev = 0, sms = 0;
+    BLP_CUDA_TRY(cudaGetDevice(&dev));
+    int rc = device_sms(dev, &sms);
+    if (rc) return rc;
+    blp::BoxBatch B{lower, upper, direction, count, n, value, point, status};
+    const long long blocks = std::min<long long>((count + 255) / 256, (long long)sms * 8);
+    blp::box_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(B);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    BLP_CUDA_TRY(cudaGetLastError());
+    return BLP_OK;
+}
+
+int blp_box_solve_host(const double *lower, const double *upper, const double *direction, int64_t count,
+                       int32_t n, double *value, double *point, int32_t *status, int32_t device) {
+    g_last_error.clear();
+    if (count < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    BLP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s;
+    BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t mat = (size_t)count * n * sizeof(double);
+    char *buf = nullptr;
+    int rc = BLP_OK;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), 4 * mat + (size_t)count * 12 + 64, s) != cudaSuccess) {
+        cudaStreamDestroy(s);
+        return fail(BLP_ERR_CUDA, "cudaMallocAsync failed");
+    }
+    double *dl = reinterpret_cast<double *>(buf), *du = dl + (size_t)count * n, *dd = du + (size_t)count * n;
+    double *dp = dd + (size_t)count * n, *dv = dp + (size_t)count * n;
+    int32_t *dst = reinterpret_cast<int32_t *>(dv + count);
+    if (mat) {
+        cudaMemcpyAsync(dl, lower, mat, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(du, upper, mat, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dd, direction, mat, cudaMemcpyHostToDevice, s);
+    }
+    rc = blp_box_solve_device(dl, du, dd, count, n, dv, dp, dst, s);
+    if (rc == BLP_OK) {
+        cudaMemcpyAsync(value, dv, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+        if (mat) cudaMemcpyAsync(point, dp, mat, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(status, dst, (size_t)count * 4, cudaMemcpyDeviceToHost, s);
+    }
+    cudaFreeAsync(buf, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc == BLP_OK && e != cudaSuccess) rc = fail(BLP_ERR_CUDA, cudaGetErrorString(e));
     return rc;
 }
 

@@ -218,3 +218,38 @@ def main(only=None):
 
 if __name__ == "__main__":
     main(set(sys.argv[1:]) or None)
+
+
+def box_records():
+    """Hyper-rectangle LPs through the reference's solve_box (boxlp.py:44-61)."""
+    from batchlp import BoxLP, InvalidBox, solve_box
+    recs = []
+
+    def add(name, lo, hi, d):
+        box = BoxLP(np.asarray(lo, float), np.asarray(hi, float), np.asarray(d, float))
+        try:
+            sol = solve_box(box)
+            out = dict(value=float(sol.value), point=[float(v) for v in sol.point])
+        except InvalidBox as err:
+            out = dict(error=str(err))
+        recs.append(dict(name=name, lower=[float(v) for v in box.lower], upper=[float(v) for v in box.upper],
+                         direction=[float(v) for v in box.direction], outcome=out))
+
+    rng = np.random.default_rng(202403)                   # test_acceptance.py:85-95
+    for k in range(300):
+        n = int(rng.integers(1, 13))
+        lower = rng.uniform(-10, 5, n)
+        add(f"crit3_{k}", lower, lower + rng.uniform(0, 10, n), rng.uniform(-5, 5, n))
+    add("zero_direction_takes_upper", [0.0, -1.0], [2.0, 3.0], [0.0, 0.0])
+    add("negative_direction_takes_lower", [1.0, -4.0], [2.0, 3.0], [-1.0, -2.0])
+    add("degenerate_box", [1.0, 1.0], [1.0, 1.0], [3.0, -3.0])
+    add("lower_above_upper", [0.0, 5.0, 1.0], [1.0, 4.0, 0.0], [1.0, 1.0, 1.0])
+    add("infinite_bound", [0.0, -np.inf], [1.0, 1.0], [1.0, 1.0])
+    add("nan_bound", [0.0, np.nan], [1.0, 1.0], [1.0, 1.0])
+    add("overflowing_sum", [1e308, 0.0], [1.7e308, 1.0], [1.0, 1.0])
+    add("empty", [], [], [])
+    return recs
+
+
+def write_box():
+    (HERE / "box.json").write_text(json.dumps(box_records(), allow_nan=True))

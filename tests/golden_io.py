@@ -84,3 +84,36 @@ def compare(got: dict, want: dict, label: str = "") -> None:
     go, wo = np.asarray(got["objective"])[opt], np.asarray(want["objective"])[opt]
     rel = np.abs(go - wo) / np.maximum(1.0, np.abs(wo))
     assert (rel <= OBJ_RTOL).all(), f"{label}: objective rel err {rel.max() if rel.size else 0}"
+
+
+def box_records() -> list[dict]:
+    return json.loads((GOLDEN / "box.json").read_text())
+
+
+def box_arrays(rec: dict):
+    lo = np.asarray(rec["lower"], np.float64)[None]
+    hi = np.asarray(rec["upper"], np.float64)[None]
+    d = np.asarray(rec["direction"], np.float64)[None]
+    return lo, hi, d
+
+
+def box_message(status: int, lo, hi) -> str | None:
+    if status == 0:
+        return None
+    if status < 0:
+        return "box bounds must be finite"
+    j = status - 1
+    return f"lower[{j}] = {lo[j]} > upper[{j}] = {hi[j]}"
+
+
+def compare_box(value, point, status, rec: dict) -> None:
+    """Points exact, values within OBJ_RTOL, errors with the reference's message."""
+    lo, hi, _ = box_arrays(rec)
+    want = rec["outcome"]
+    if "error" in want:
+        assert status != 0, rec["name"]
+        assert box_message(int(status), lo[0], hi[0]) == want["error"], rec["name"]
+        return
+    assert status == 0, f"{rec['name']}: status {status}"
+    assert np.array_equal(np.asarray(point), np.asarray(want["point"])), rec["name"]
+    assert abs(value - want["value"]) <= OBJ_RTOL * max(1.0, abs(want["value"])), rec["name"]

@@ -170,3 +170,40 @@ def test_iteration_limit_and_trigger_limits_flow_through():
                 dict(anti_cycling=False, max_iterations=400)):
         res = batch_solve_arrays(A, b, c, SolverLimits(**lim))
         compare(_native_dict(res), oracle.solve_batch(A, b, c, **lim), f"limits {lim}")
+
+
+def test_box_records_match_reference():
+    """Batched hyper-rectangle LPs (the paper's Eq. 7 kernel) vs the reference's solve_box."""
+    from golden_io import box_arrays, box_records, compare_box
+    from paper_1802_08557_b200 import BoxLP, InvalidBox, box_batch_arrays, solve_box, solve_box_batch
+    recs = box_records()
+    for rec in recs:
+        lo, hi, d = box_arrays(rec)
+        r = box_batch_arrays(lo, hi, d)
+        compare_box(r.value[0], r.point[0], r.status[0], rec)
+    boxes = [BoxLP.build(r["lower"], r["upper"], r["direction"]) for r in recs]
+    got = solve_box_batch(boxes)
+    for rec, g in zip(recs, got):
+        if "error" in rec["outcome"]:
+            assert isinstance(g, InvalidBox) and str(g) == rec["outcome"]["error"]
+        else:
+            assert np.array_equal(g.point, np.asarray(rec["outcome"]["point"]))
+    with pytest.raises(InvalidBox, match="box bounds must be finite"):
+        solve_box(BoxLP.build([0.0], [np.inf], [1.0]))
+
+
+def test_box_batch_1e5_against_oracle():
+    """Criterion-3 batch shape: 1e5 boxes of dimension 5 (test_acceptance.py:96-104)."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import box_batch_arrays
+    rng = np.random.default_rng(77)
+    lo = rng.uniform(-5, 5, (100_000, 5))
+    hi = lo + rng.uniform(0, 5, (100_000, 5))
+    d = rng.uniform(-3, 3, (100_000, 5))
+    lo[17, 2], hi[17, 2] = 3.0, 1.0
+    r = box_batch_arrays(lo, hi, d)
+    w = oracle.box_solve(lo[:2000], hi[:2000], d[:2000])
+    assert np.array_equal(r.status[:2000], w["status"]) and np.array_equal(r.point[:2000], w["point"])
+    ok = w["status"] == 0
+    assert np.allclose(r.value[:2000][ok], w["value"][ok], rtol=1e-12, atol=0)
+    assert (r.status == 0).sum() == 100_000 - 1 and r.status[17] == 3

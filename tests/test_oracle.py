@@ -57,3 +57,11 @@ def test_oracle_against_live_reference(reference):
                     objective=[out.objective_value if out.objective_value is not None else np.nan],
                     x=[out.primal_point if out.primal_point is not None else np.zeros(n)])
         compare(got, want, f"live{k}")
+
+
+def test_box_oracle_matches_reference():
+    from golden_io import box_arrays, box_records, compare_box
+    for rec in box_records():
+        lo, hi, d = box_arrays(rec)
+        r = oracle.box_solve(lo, hi, d)
+        compare_box(r["value"][0], r["point"][0], r["status"][0], rec)
