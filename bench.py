@@ -244,10 +244,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # One process per GPU.  BLP_BENCH_SHARE_GPU=1 folds ranks onto the visible GPUs and uses
+    # gloo for the scalar collectives: a functional check of the multi-rank path on a 1-GPU box.
+    share = os.environ.get("BLP_BENCH_SHARE_GPU") == "1"
+    local_dev = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     A, b, c, shared, spec = workload(args.config, args.count, rank)
     count, n = c.shape
@@ -282,7 +289,7 @@ def main():
     # ---- device-resident value: CUDA events per step on the launching stream ----
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = _native.launch_count()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         barrier()
         t_all0 = torch.cuda.Event(enable_timing=True)
         t_all1 = torch.cuda.Event(enable_timing=True)
@@ -305,14 +312,14 @@ def main():
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device='cpu' if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device='cpu' if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -328,9 +335,9 @@ def main():
     fpp = 2 * (m + 1) * (n + m + 1)
     secs = step_ms / 1e3
     achieved_gbs = pivots * bpp / secs / 1e9
-    smem_peak = _native.probe_smem_gbs(local)
+    smem_peak = _native.probe_smem_gbs(local_dev)
     hbm_peak, hbm_src = measured_hbm_gbs()
-    fp64_peak = _native.probe_fp64_gflops(local) / 1e3
+    fp64_peak = _native.probe_fp64_gflops(local_dev) / 1e3
     # On-chip-resident tableaux (registers or shared memory) are judged against the
     # measured shared-memory bandwidth, BASELINE.md §2's roofline for C1-C4; the
     # register variants would only switch to the FP64 bound past 100% of it

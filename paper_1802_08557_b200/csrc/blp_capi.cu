@@ -127,6 +127,8 @@ bool plan_warplp(int m, int n, Plan *p) {
     if (m > 32) return false;
     if (ncols <= 32) {
         p->fn = blp::warplp_kernel<32, 16>; p->name = "warplp_c32"; p->smem = blp::WlpCfg<32>::bytes(m);
+    } else if (ncols <= 62 && env_int("BLP_WLP_C62", 1)) {
+        p->fn = blp::warplp_kernel<62, 12>; p->name = "warplp_c62"; p->smem = blp::WlpCfg<62>::bytes(m);
     } else if (ncols <= 64) {
         // BLP_WLP_MINB trades registers (= ILP) against resident LPs per SM
         switch (env_int("BLP_WLP_MINB", 12)) {

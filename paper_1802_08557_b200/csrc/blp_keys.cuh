@@ -62,7 +62,7 @@ struct RegPicker {
             return v;
         } else {
             if (i < LO + N / 2) return RegPicker<LO, N / 2, CPW>::get(a, i);
-            return RegPicker<LO + N / 2, N / 2, CPW>::get(a, i);
+            return RegPicker<LO + N / 2, N - N / 2, CPW>::get(a, i);
         }
     }
 };

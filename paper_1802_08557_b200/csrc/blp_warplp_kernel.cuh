@@ -24,7 +24,7 @@ namespace blp {
 
 template <int CPW>
 struct WlpCfg {
-    static constexpr int OPW = CPW / 32;
+    static constexpr int OPW = (CPW + 31) / 32;
     static constexpr int LDG = CPW + 1;            // odd stage row stride: conflict-free transposes
     static constexpr size_t ROWBUF = 0;            // CPW doubles
     static constexpr size_t RVEC = ROWBUF + CPW * 8;
@@ -37,7 +37,7 @@ enum { kWlpRestore = 0, kWlpPhase1 = 1, kWlpPhase2 = 2 };
 
 template <int CPW>
 struct WlpState {
-    static constexpr int OPW = CPW / 32;
+    static constexpr int OPW = (CPW + 31) / 32;
     double a[CPW];          // constraint row `lane` (zero for lanes >= m)
     double rc[OPW];         // transposed objective row; position 0 holds the objective value
     double arc[OPW];        // phase-1 reduced cost of the artificial paired with a slack position
