@@ -20,6 +20,7 @@
 #include "blp_common.cuh"
 #include "blp_regtile_kernel.cuh"
 #include "blp_warplp_kernel.cuh"
+#include "blp_warplp2_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 #include "blp_box_kernel.cuh"
 
@@ -127,7 +128,22 @@ bool plan_warplp(int m, int n, Plan *p) {
     if (m > 32) return false;
     if (ncols <= 32) {
         p->fn = blp::warplp_kernel<32, 16>; p->name = "warplp_c32"; p->smem = blp::WlpCfg<32>::bytes(m);
-    } else if (ncols <= 62 && env_int("BLP_WLP_C62", 1)) {
+    } else if (ncols <= 62 && env_int("BLP_WLP2", 38) > 0) {
+        // register/smem split row (blp_warplp2_kernel.cuh); BLP_WLP2 = register columns
+        // (C2 1e5: r38/s24 @16 LPs/SM 8.9 ms, r46/s16 9.8, r30/s32 10.1, all-register c62 10.3)
+        switch (env_int("BLP_WLP2", 38)) {
+            case 30: p->fn = blp::warplp2_kernel<30, 32, 18>; p->name = "warplp2_r30_s32";
+                     p->smem = blp::Wl2Cfg<30, 32>::BYTES; break;
+            case 34: p->fn = blp::warplp2_kernel<34, 28, 17>; p->name = "warplp2_r34_s28";
+                     p->smem = blp::Wl2Cfg<34, 28>::BYTES; break;
+            case 42: p->fn = blp::warplp2_kernel<42, 20, 15>; p->name = "warplp2_r42_s20";
+                     p->smem = blp::Wl2Cfg<42, 20>::BYTES; break;
+            case 46: p->fn = blp::warplp2_kernel<46, 16, 14>; p->name = "warplp2_r46_s16";
+                     p->smem = blp::Wl2Cfg<46, 16>::BYTES; break;
+            default: p->fn = blp::warplp2_kernel<38, 24, 16>; p->name = "warplp2_r38_s24";
+                     p->smem = blp::Wl2Cfg<38, 24>::BYTES; break;
+        }
+    } else if (ncols <= 62) {
         p->fn = blp::warplp_kernel<62, 12>; p->name = "warplp_c62"; p->smem = blp::WlpCfg<62>::bytes(m);
     } else if (ncols <= 64) {
         // BLP_WLP_MINB trades registers (= ILP) against resident LPs per SM
