@@ -397,7 +397,7 @@ def main():
         "e2e": {"value": total_lps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                 "h2d_pinned_gbs": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6,
-                "api": "batch_solve_arrays (blp_solve_batch_host, 3-stream pipelined sub-batches)"},
+                "api": "batch_solve_arrays (blp_solve_batch_host: 32 sub-batches pipelined over 4 streams)"},
         "gpu_launches": int(launches),
         "timed_region_ms": region_ms,
         "clocks": clocks.summary(),
