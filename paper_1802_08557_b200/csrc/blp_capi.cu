@@ -21,6 +21,7 @@
 #include "blp_regtile_kernel.cuh"
 #include "blp_warplp_kernel.cuh"
 #include "blp_warplp2_kernel.cuh"
+#include "blp_pairlp_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 #include "blp_box_kernel.cuh"
 
@@ -161,11 +162,32 @@ bool plan_warplp(int m, int n, Plan *p) {
     return true;
 }
 
-// BLP_KERNEL=warplp|regtile|smem forces a family (testing / tuning).
+// Two-warp-per-LP variant: 32 < m <= 64 rows, n + m + 1 <= R + S columns (C4).
+// BLP_PAIR = register columns per row.
+bool plan_pairlp(int m, int n, Plan *p) {
+    const int ncols = n + m + 1;
+    if (m <= 32 || m > 64) return false;
+    switch (env_int("BLP_PAIR", 62)) {
+        case 50:
+            if (ncols > 98) return false;
+            p->fn = blp::pairlp_kernel<50, 48, 7>; p->name = "pairlp_r50_s48"; p->smem = blp::PairCfg<50, 48>::BYTES;
+            break;
+        default:
+            if (ncols > 98) return false;
+            p->fn = blp::pairlp_kernel<62, 36, 6>; p->name = "pairlp_r62_s36"; p->smem = blp::PairCfg<62, 36>::BYTES;
+            break;
+    }
+    p->threads = 64;
+    p->slot = 0;
+    return true;
+}
+
+// BLP_KERNEL=warplp|pairlp|regtile|smem forces a family (testing / tuning).
 bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
     if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
+    if ((any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p)) return true;
     if ((any || strcmp(force, "warplp") == 0 || strcmp(force, "regtile") == 0) && plan_regtile(m, n, p)) return true;
     return plan_tableau(m, n, p);
 }
