@@ -162,24 +162,34 @@ bool plan_warplp(int m, int n, Plan *p) {
     return true;
 }
 
-// Two-warp-per-LP variant: 32 < m <= 64 rows, n + m + 1 <= R + S columns (C4).
-// BLP_PAIR = register columns per row.
-bool plan_pairlp(int m, int n, Plan *p) {
-    const int ncols = n + m + 1;
-    if (m <= 32 || m > 64) return false;
-    switch (env_int("BLP_PAIR", 62)) {
-        case 50:
-            if (ncols > 98) return false;
-            p->fn = blp::pairlp_kernel<50, 48, 7>; p->name = "pairlp_r50_s48"; p->smem = blp::PairCfg<50, 48>::BYTES;
-            break;
-        default:
-            if (ncols > 98) return false;
-            p->fn = blp::pairlp_kernel<62, 36, 6>; p->name = "pairlp_r62_s36"; p->smem = blp::PairCfg<62, 36>::BYTES;
-            break;
-    }
-    p->threads = 64;
+// Row-warp-per-LP variants (blp_pairlp_kernel.cuh): NWR warps own 32 rows each, a row's
+// first R positions in registers and the next S in a [S][ST] shared tile (ST >= m).
+template <int R, int S, int NWR, int ST, int MINB>
+bool use_pairlp(int m, int ncols, const char *name, Plan *p) {
+    if (m > ST || ncols > R + S) return false;
+    p->fn = blp::pairlp_kernel<R, S, NWR, ST, MINB>;
+    p->name = name;
+    p->smem = blp::PairCfg<R, S, NWR, ST>::BYTES;
+    p->threads = 32 * NWR;
     p->slot = 0;
     return true;
+}
+
+// 32 < m <= 64: two row-warps (C4 64 x 32); 64 < m <= 128: four (C3 100 x 100), 2 LPs per SM.
+// BLP_PAIR / BLP_QUAD = register columns per row.
+bool plan_pairlp(int m, int n, Plan *p) {
+    const int ncols = n + m + 1;
+    if (m > 64 && m <= 128) {
+        switch (env_int("BLP_QUAD", 80)) {
+            case 64: if (use_pairlp<64, 138, 4, 100, 2>(m, ncols, "quadlp_r64_s138", p)) return true; break;
+            case 96: break;
+            default: if (use_pairlp<80, 122, 4, 100, 2>(m, ncols, "quadlp_r80_s122", p)) return true; break;
+        }
+        return use_pairlp<96, 106, 4, 128, 2>(m, ncols, "quadlp_r96_s106", p);
+    }
+    if (m <= 32 || m > 64) return false;
+    if (env_int("BLP_PAIR", 62) == 50) return use_pairlp<50, 48, 2, 64, 7>(m, ncols, "pairlp_r50_s48", p);
+    return use_pairlp<62, 36, 2, 64, 6>(m, ncols, "pairlp_r62_s36", p);
 }
 
 // BLP_KERNEL=warplp|pairlp|regtile|smem forces a family (testing / tuning).

@@ -93,6 +93,20 @@ __device__ __forceinline__ double selp_f64(double a, double b, bool p) {
     return r;
 }
 
+// Ordered shared-memory accesses (volatile: emitted in program order), used
+// where a hand-pipelined loop must keep its loads ahead of earlier stores.
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void lds_v2_f64(unsigned addr, double &x, double &y) {
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ double div_entry(double a, double b) {
     const bool z = a == 0.0;
     const double q = __ddiv_rn(selp_f64(1.0, a, z), b);

@@ -207,3 +207,32 @@ def test_box_batch_1e5_against_oracle():
     ok = w["status"] == 0
     assert np.allclose(r.value[:2000][ok], w["value"][ok], rtol=1e-12, atol=0)
     assert (r.status == 0).sum() == 100_000 - 1 and r.status[17] == 3
+
+
+FAMILY_SHAPES = [(3, 5), (12, 19), (28, 32), (30, 31), (31, 32), (32, 32), (33, 20), (40, 50), (64, 33),
+                 (64, 34), (65, 8), (100, 100), (128, 73), (128, 74), (90, 140)]
+
+
+@pytest.mark.parametrize("m,n", FAMILY_SHAPES)
+def test_every_kernel_family_matches_oracle(m, n, monkeypatch):
+    """Shapes on both sides of each kernel-family boundary, every applicable family forced
+    (BLP_KERNEL / BLP_FORCE_HBM), each equal to the oracle: afiro-style two-phase LPs plus the
+    degenerate / unbounded / infeasible / padded-Beale mix."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, batch_solve_arrays, workloads
+    A1, b1, c1 = workloads.afiro_arrays(200, seed=m * 1000 + n, m=m, n=n)
+    A2, b2, c2 = workloads.degenerate_arrays(300, seed=m * 1000 + n + 1, m=m, n=n)
+    A, b, c = (np.concatenate(v) for v in ((A1, A2), (b1, b2), (c1, c2)))
+    want = oracle.solve_batch(A, b, c)
+    seen = set()
+    for force, hbm in (("", "0"), ("warplp", "0"), ("pairlp", "0"), ("regtile", "0"), ("smem", "0"),
+                       ("smem", "1")):
+        monkeypatch.setenv("BLP_KERNEL", force)
+        monkeypatch.setenv("BLP_FORCE_HBM", hbm)
+        variant = _native.kernel_variant(m, n)
+        if variant in seen:
+            continue
+        seen.add(variant)
+        res = batch_solve_arrays(A, b, c)
+        compare(_native_dict(res), want, f"({m},{n}) {variant}")
+    assert seen
