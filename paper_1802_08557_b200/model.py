@@ -6,7 +6,8 @@ Restates the hot-path subset of the reference data model
 (:126-141) and ``validate`` (:263-301), with the same field names, string
 values and violation messages so callers and tests written against the
 reference work unchanged.  General-form lowering (GeneralLP, standardize,
-VariableMap) is host-side ingest outside the batched path.
+VariableMap) and the MPS reader are host-side ingest in general.py / mps.py
+(SURVEY.md §8(f) row 2).
 
 The batch path does not call ``validate`` per LP: the kernels flag non-finite
 inputs while building the tableau (BLP_STATUS_INVALID) and ``validate`` is

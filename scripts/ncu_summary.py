@@ -23,6 +23,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("rep")
 ap.add_argument("--config", required=True)
 ap.add_argument("--lps", type=int, required=True)
+ap.add_argument("--variant", default=None, help="blp_kernel_variant name (bench.py looks traffic up by it)")
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -58,7 +59,7 @@ for t in traffic:
         variant = "regtile"
     elif "tableau_kernel" in k:
         variant = ("smem" if "(bool)1" in k else "hbm")
-    t["variant_family"] = variant
+    t["variant_family"] = a.variant or variant
 tj = Path("profiles/traffic.json")
 recs = json.loads(tj.read_text()) if tj.exists() else []
 for t in traffic:

@@ -236,3 +236,38 @@ def test_every_kernel_family_matches_oracle(m, n, monkeypatch):
         res = batch_solve_arrays(A, b, c)
         compare(_native_dict(res), want, f"({m},{n}) {variant}")
     assert seen
+
+
+def test_general_form_batches_match_reference():
+    """General-form ingest (MPS fixtures + seeded general LPs) -> packed GPU batches per lowered
+    shape -> recover_batch, vs the reference's standardize / solve / recover_outcome."""
+    import json
+    from golden_io import GOLDEN, OBJ_RTOL
+    from paper_1802_08557_b200 import GeneralLP, batch_solve_general, lower_to_general, parse_mps
+
+    def glp_of(g):
+        return GeneralLP.build(g["sense"], g["c"], np.asarray(g["rows"]).reshape(g["k"], g["n"]), g["relations"],
+                               g["rhs"], g["lower"], g["upper"], g["row_names"], g["col_names"])
+
+    items = []
+    for r in json.loads((GOLDEN / "general.json").read_text())["records"]:
+        if "error" not in r["lowered"]:
+            items.append((r["name"], glp_of(r["general"]), r["lowered"]))
+    for r in json.loads((GOLDEN / "mps.json").read_text())["records"]:
+        if "lowered" in r and "error" not in r["lowered"]:
+            items.append((r["name"], lower_to_general(parse_mps(r["text"])), r["lowered"]))
+    groups = {}
+    for it in items:
+        groups.setdefault((it[2]["m"], it[2]["n"]), []).append(it)
+    checked = 0
+    for shape, group in groups.items():
+        got = batch_solve_general([g for _, g, _ in group])
+        for k, (name, _, want) in enumerate(group):
+            w = want["outcome"]
+            assert got.status[k] == w["status"], name
+            assert (got.iterations_phase1[k], got.iterations_phase2[k]) == (want["std"]["it1"], want["std"]["it2"]), name
+            if w["status"] == 0:
+                assert np.array_equal(got.x[k], np.asarray(w["x"])), name
+                assert abs(got.objective[k] - w["objective"]) <= OBJ_RTOL * max(1.0, abs(w["objective"])), name
+            checked += 1
+    assert checked > 650
