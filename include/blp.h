@@ -116,6 +116,40 @@ int blp_box_solve_host(const double *lower, const double *upper, const double *d
                        int64_t count, int32_t n, double *value, double *point, int32_t *status,
                        int32_t device);
 
+/*
+ * Batched from-scratch optimality certificates (
+ * replaces the reference's per-LP oracle.py:168-223 check_certificate).
+ * For each LP k with status[k] == 0 (OPTIMAL), from A, b, c and the point
+ * x [count][n] only: max_violation = max(0, max(A x - b)), max_negativity =
+ * max(0, max(-x)), and max_reduced_cost = max(c_ext - [A|I]^T y) with y the
+ * duals of a basis rebuilt greedily from the point's support (levels > tol
+ * first, then the rest, index order, rank test at numpy's SVD threshold).
+ * needs_prices[k] = 1 when max_reduced_cost > tol on a primal-feasible point:
+ * the reference then looks for complementary-slackness prices with an
+ * auxiliary LP (oracle.py:226-242), which the caller solves with
+ * blp_solve_batch_* and applies through blp_certify_reprice_*.
+ * Non-OPTIMAL LPs get NaN outputs and needs_prices 0.
+ */
+int blp_certify_batch_device(const double *A, const double *b, const double *c, const double *x,
+                             int64_t count, int32_t m, int32_t n, int32_t shared_Ab,
+                             const int8_t *status, double tol,
+                             double *max_reduced_cost, double *max_violation, double *max_negativity,
+                             int8_t *needs_prices, void *cuda_stream);
+int blp_certify_batch_host(const double *A, const double *b, const double *c, const double *x,
+                           int64_t count, int32_t m, int32_t n, int32_t shared_Ab,
+                           const int8_t *status, double tol,
+                           double *max_reduced_cost, double *max_violation, double *max_negativity,
+                           int8_t *needs_prices, int32_t device);
+
+/* max_reduced_cost[k] = max(c - A^T y_k, -y_k) for every k with mask[k] != 0
+ * (y [count][m]: complementary prices; oracle.py:220-222). */
+int blp_certify_reprice_device(const double *A, const double *c, const double *y, int64_t count,
+                               int32_t m, int32_t n, int32_t shared_Ab, const int8_t *mask,
+                               double *max_reduced_cost, void *cuda_stream);
+int blp_certify_reprice_host(const double *A, const double *c, const double *y, int64_t count,
+                             int32_t m, int32_t n, int32_t shared_Ab, const int8_t *mask,
+                             double *max_reduced_cost, int32_t device);
+
 /* Largest (m, n) the library accepts: 1 if supported, 0 otherwise. */
 int blp_shape_supported(int32_t m, int32_t n);
 

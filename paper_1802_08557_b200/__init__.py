@@ -27,6 +27,7 @@ from .batch import (
     support_batch,
 )
 from .boxlp import BoxArrays, BoxLP, BoxSolution, InvalidBox, box_batch_arrays, solve_box, solve_box_batch
+from .certify import ORACLE_TOL, Certificate, CertificateBatch, certify_batch, check_certificate
 from .general import (GeneralBatch, GeneralLP, InfeasibleBounds, Relation, Sense, VariableMap,
                       batch_solve_general, recover_batch, solve_general, standardize, standardize_batch)
 from .model import SolveOutcome, StandardFormLP, Status, standard_form, validate
@@ -44,6 +45,7 @@ __all__ = [
     "GeneralBatch", "GeneralLP", "InfeasibleBounds", "MpsModel", "ParseError", "Relation", "Sense",
     "UnsupportedFeature", "VariableMap", "batch_solve_general", "lower_to_general", "parse_mps",
     "recover_batch", "solve_general", "standardize", "standardize_batch",
+    "ORACLE_TOL", "Certificate", "CertificateBatch", "certify_batch", "check_certificate",
 ]
 
 __version__ = "0.1.0"

@@ -41,7 +41,9 @@ _lib = None
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
 EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
            "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
-           "blp_probe_smem_gbs", "blp_probe_fp64_gflops", "blp_box_solve_device", "blp_box_solve_host")
+           "blp_probe_smem_gbs", "blp_probe_fp64_gflops", "blp_box_solve_device", "blp_box_solve_host",
+           "blp_certify_batch_device", "blp_certify_batch_host", "blp_certify_reprice_device",
+           "blp_certify_reprice_host")
 
 
 def load():
@@ -79,6 +81,17 @@ def load():
     lib.blp_box_solve_device.restype = ctypes.c_int
     lib.blp_box_solve_host.argtypes = box + [ctypes.c_int32]
     lib.blp_box_solve_host.restype = ctypes.c_int
+    cert = [P, P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, ctypes.c_double,
+            P, P, P, P]
+    lib.blp_certify_batch_device.argtypes = cert + [P]
+    lib.blp_certify_batch_device.restype = ctypes.c_int
+    lib.blp_certify_batch_host.argtypes = cert + [ctypes.c_int32]
+    lib.blp_certify_batch_host.restype = ctypes.c_int
+    rep = [P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P]
+    lib.blp_certify_reprice_device.argtypes = rep + [P]
+    lib.blp_certify_reprice_device.restype = ctypes.c_int
+    lib.blp_certify_reprice_host.argtypes = rep + [ctypes.c_int32]
+    lib.blp_certify_reprice_host.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -92,6 +105,31 @@ def box_solve_host(lower: np.ndarray, upper: np.ndarray, direction: np.ndarray, 
     _check(lib.blp_box_solve_host(_ptr(lower), _ptr(upper), _ptr(direction), count, n, _ptr(out["value"]),
                                   _ptr(out["point"]), _ptr(out["status"]), int(device)))
     return out
+
+
+def certify_host(A, b, c, x, status, tol: float, *, shared_Ab: bool = False, device: int = 0) -> dict:
+    """Batched certificates of packed LPs + points (blp_certify_batch_host)."""
+    lib = load()
+    _require_gpu()
+    count, n = c.shape
+    m = b.shape[-1]
+    out = dict(max_reduced_cost=np.empty(count), max_violation=np.empty(count), max_negativity=np.empty(count),
+               needs_prices=np.empty(count, np.int8))
+    _check(lib.blp_certify_batch_host(_ptr(A), _ptr(b), _ptr(c), _ptr(x), count, m, n, int(shared_Ab),
+                                      _ptr(status), float(tol), _ptr(out["max_reduced_cost"]),
+                                      _ptr(out["max_violation"]), _ptr(out["max_negativity"]),
+                                      _ptr(out["needs_prices"]), int(device)))
+    return out
+
+
+def certify_reprice_host(A, c, y, mask, max_reduced_cost, *, shared_Ab: bool = False, device: int = 0) -> None:
+    """In place: max_reduced_cost[k] = max(c - A^T y_k, -y_k) where mask[k] (blp_certify_reprice_host)."""
+    lib = load()
+    _require_gpu()
+    count, n = c.shape
+    m = y.shape[-1]
+    _check(lib.blp_certify_reprice_host(_ptr(A), _ptr(c), _ptr(y), count, m, n, int(shared_Ab), _ptr(mask),
+                                        _ptr(max_reduced_cost), int(device)))
 
 
 def _check(rc: int) -> None:

@@ -24,6 +24,7 @@
 #include "blp_pairlp_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 #include "blp_box_kernel.cuh"
+#include "blp_cert_kernel.cuh"
 
 namespace {
 
@@ -560,4 +561,129 @@ int blp_box_solve_host(const double *lower, const double *upper, const double *d
     return rc;
 }
 
+int blp_certify_batch_device(const double *A, const double *b, const double *c, const double *x, int64_t count,
+                             int32_t m, int32_t n, int32_t shared_Ab, const int8_t *status, double tol,
+                             double *max_reduced_cost, double *max_violation, double *max_negativity,
+                             int8_t *needs_prices, void *cuda_stream) {
+    g_last_error.clear();
+    if (count < 0 || m < 0 || n < 0 || (count > 0 && (!c || !x || !status || !max_reduced_cost || !max_violation ||
+                                                     !max_negativity || !needs_prices || (m > 0 && (!A || !b)))))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    int dev = 0, sms = 0;
+    BLP_CUDA_TRY(cudaGetDevice(&dev));
+    int rc = device_sms(dev, &sms);
+    if (rc) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(cuda_stream);
+    const size_t per_cta = (size_t)2 * m * m * sizeof(double);
+    long long grid = std::min<long long>(count, (long long)sms * 8);
+    if (per_cta) grid = std::max<long long>(1, std::min<long long>(grid, (1ll << 30) / (long long)per_cta));
+    double *work = nullptr;
+    if (per_cta && cudaMallocAsync(reinterpret_cast<void **>(&work), per_cta * grid, s) != cudaSuccess)
+        return fail(BLP_ERR_CUDA, "cudaMallocAsync (certificate workspace) failed");
+    const size_t smem = ((size_t)2 * n + 9 * (size_t)m + 32) * sizeof(double);
+    if (smem > 48 * 1024) BLP_CUDA_TRY(cudaFuncSetAttribute(blp::cert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    blp::CertBatch B{A, b, c, x, count, m, n, shared_Ab, status, tol, max_reduced_cost, max_violation, max_negativity,
+                     needs_prices, work};
+    blp::cert_kernel<<<(unsigned)grid, blp::kCertThreads, smem, s>>>(B);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (work) cudaFreeAsync(work, s);
+    if (e != cudaSuccess) return fail(BLP_ERR_CUDA, cudaGetErrorString(e));
+    return BLP_OK;
+}
+
+int blp_certify_batch_host(const double *A, const double *b, const double *c, const double *x, int64_t count,
+                           int32_t m, int32_t n, int32_t shared_Ab, const int8_t *status, double tol,
+                           double *max_reduced_cost, double *max_violation, double *max_negativity,
+                           int8_t *needs_prices, int32_t device) {
+    g_last_error.clear();
+    if (count < 0 || m < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    BLP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s;
+    BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t na = (shared_Ab ? 1 : (size_t)count) * m * n, nb = (shared_Ab ? 1 : (size_t)count) * m;
+    const size_t nc = (size_t)count * n;
+    const size_t doubles = na + nb + 2 * nc + 3 * (size_t)count;
+    char *buf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), doubles * 8 + 2 * (size_t)count + 64, s) != cudaSuccess) {
+        cudaStreamDestroy(s);
+        return fail(BLP_ERR_CUDA, "cudaMallocAsync failed");
+    }
+    double *dA = reinterpret_cast<double *>(buf), *db = dA + na, *dc = db + nb, *dx = dc + nc;
+    double *drc = dx + nc, *dv = drc + count, *dn = dv + count;
+    int8_t *dst = reinterpret_cast<int8_t *>(dn + count), *dneed = dst + count;
+    if (na) cudaMemcpyAsync(dA, A, na * 8, cudaMemcpyHostToDevice, s);
+    if (nb) cudaMemcpyAsync(db, b, nb * 8, cudaMemcpyHostToDevice, s);
+    if (nc) {
+        cudaMemcpyAsync(dc, c, nc * 8, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dx, x, nc * 8, cudaMemcpyHostToDevice, s);
+    }
+    cudaMemcpyAsync(dst, status, (size_t)count, cudaMemcpyHostToDevice, s);
+    int rc = blp_certify_batch_device(dA, db, dc, dx, count, m, n, shared_Ab, dst, tol, drc, dv, dn, dneed, s);
+    if (rc == BLP_OK) {
+        cudaMemcpyAsync(max_reduced_cost, drc, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(max_violation, dv, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(max_negativity, dn, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(needs_prices, dneed, (size_t)count, cudaMemcpyDeviceToHost, s);
+    }
+    cudaFreeAsync(buf, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc == BLP_OK && e != cudaSuccess) rc = fail(BLP_ERR_CUDA, cudaGetErrorString(e));
+    return rc;
+}
+
+int blp_certify_reprice_device(const double *A, const double *c, const double *y, int64_t count, int32_t m,
+                               int32_t n, int32_t shared_Ab, const int8_t *mask, double *max_reduced_cost,
+                               void *cuda_stream) {
+    g_last_error.clear();
+    if (count < 0 || m < 0 || n < 0 || (count > 0 && (!c || !mask || !max_reduced_cost || (m > 0 && (!A || !y)))))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    int dev = 0, sms = 0;
+    BLP_CUDA_TRY(cudaGetDevice(&dev));
+    int rc = device_sms(dev, &sms);
+    if (rc) return rc;
+    blp::CertPrices P{A, c, y, count, m, n, shared_Ab, mask, max_reduced_cost};
+    const long long blocks = std::min<long long>((count + 7) / 8, (long long)sms * 8);
+    blp::cert_prices_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(P);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    BLP_CUDA_TRY(cudaGetLastError());
+    return BLP_OK;
+}
+
+int blp_certify_reprice_host(const double *A, const double *c, const double *y, int64_t count, int32_t m,
+                             int32_t n, int32_t shared_Ab, const int8_t *mask, double *max_reduced_cost,
+                             int32_t device) {
+    g_last_error.clear();
+    if (count < 0 || m < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    BLP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s;
+    BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t na = (shared_Ab ? 1 : (size_t)count) * m * n, nc = (size_t)count * n, ny = (size_t)count * m;
+    char *buf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&buf), (na + nc + ny + count) * 8 + count + 64, s) != cudaSuccess) {
+        cudaStreamDestroy(s);
+        return fail(BLP_ERR_CUDA, "cudaMallocAsync failed");
+    }
+    double *dA = reinterpret_cast<double *>(buf), *dc = dA + na, *dy = dc + nc, *drc = dy + ny;
+    int8_t *dmask = reinterpret_cast<int8_t *>(drc + count);
+    if (na) cudaMemcpyAsync(dA, A, na * 8, cudaMemcpyHostToDevice, s);
+    if (nc) cudaMemcpyAsync(dc, c, nc * 8, cudaMemcpyHostToDevice, s);
+    if (ny) cudaMemcpyAsync(dy, y, ny * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(drc, max_reduced_cost, (size_t)count * 8, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dmask, mask, (size_t)count, cudaMemcpyHostToDevice, s);
+    int rc = blp_certify_reprice_device(dA, dc, dy, count, m, n, shared_Ab, dmask, drc, s);
+    if (rc == BLP_OK) cudaMemcpyAsync(max_reduced_cost, drc, (size_t)count * 8, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(buf, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc == BLP_OK && e != cudaSuccess) rc = fail(BLP_ERR_CUDA, cudaGetErrorString(e));
+    return rc;
+}
+
 }  // extern "C"
+

@@ -238,6 +238,7 @@ def test_every_kernel_family_matches_oracle(m, n, monkeypatch):
     assert seen
 
 
+@pytest.mark.filterwarnings("ignore::UserWarning")   # the edge-case MPS texts warn by design
 def test_general_form_batches_match_reference():
     """General-form ingest (MPS fixtures + seeded general LPs) -> packed GPU batches per lowered
     shape -> recover_batch, vs the reference's standardize / solve / recover_outcome."""
