@@ -274,6 +274,7 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
     if not lps:
         return BatchReport(outcomes=[], plan=plan, chunk_seconds=[], total_seconds=0.0)
 
+    started = time.perf_counter()        # like batch.py:157, the timer covers everything after planning
     # Pack once.  The reference raises at the first invalid LP in index order
     # (validate() inside solve()); a mis-shaped A stops packing there, and
     # non-finite entries are flagged by the kernel (BLP_STATUS_INVALID).
@@ -296,7 +297,6 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
 
     outcomes: list[SolveOutcome | None] = [None] * len(lps)
     chunk_seconds: list[float] = []
-    started = time.perf_counter()
     for start, end in plan.bounds:
         t0 = time.perf_counter()
         res = _solve_sharded(A[start:end], b[start:end], c[start:end], config.limits,

@@ -181,16 +181,13 @@ bool use_pairlp(int m, int ncols, const char *name, Plan *p) {
 bool plan_pairlp(int m, int n, Plan *p) {
     const int ncols = n + m + 1;
     if (m > 64 && m <= 128) {
-        switch (env_int("BLP_QUAD", 80)) {
-            case 64: if (use_pairlp<64, 138, 4, 100, 2>(m, ncols, "quadlp_r64_s138", p)) return true; break;
-            case 96: break;
-            default: if (use_pairlp<80, 122, 4, 100, 2>(m, ncols, "quadlp_r80_s122", p)) return true; break;
-        }
-        return use_pairlp<96, 106, 4, 128, 2>(m, ncols, "quadlp_r96_s106", p);
+        if (env_int("BLP_QUAD", 80) != 96 && use_pairlp<80, 122, 4, 101, 2>(m, ncols, "quadlp_r80_s122", p))
+            return true;
+        return use_pairlp<96, 106, 4, 129, 2>(m, ncols, "quadlp_r96_s106", p);
     }
     if (m <= 32 || m > 64) return false;
-    if (env_int("BLP_PAIR", 62) == 50) return use_pairlp<50, 48, 2, 64, 7>(m, ncols, "pairlp_r50_s48", p);
-    return use_pairlp<62, 36, 2, 64, 6>(m, ncols, "pairlp_r62_s36", p);
+    if (env_int("BLP_PAIR", 62) == 50) return use_pairlp<50, 48, 2, 65, 7>(m, ncols, "pairlp_r50_s48", p);
+    return use_pairlp<62, 36, 2, 65, 6>(m, ncols, "pairlp_r62_s36", p);
 }
 
 // BLP_KERNEL=warplp|pairlp|regtile|smem forces a family (testing / tuning).

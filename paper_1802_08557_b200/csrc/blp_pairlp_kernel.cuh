@@ -25,7 +25,9 @@ struct PairCfg {
     static constexpr int CPW = R + S;
     static constexpr int ROWS = 32 * NWR;
     static constexpr int OPW = (CPW + ROWS - 1) / ROWS;             // transposed slots per lane
-    static_assert(ST <= ROWS, "tile stride covers at most the CTA's rows");
+    // ST (>= m, checked by the planner) is odd so that a row read across columns
+    // (lane q -> tile[q][l], the pivot row's division) is bank-conflict free
+    static_assert(ST <= ROWS + 1 && (ST & 1), "odd tile stride, at most one padding row");
     static constexpr size_t TILE = 0;                               // S x ST doubles, tile[c][row]
     static constexpr size_t ROWBUF = TILE + (size_t)S * ST * 8;     // R doubles
     static constexpr size_t RVEC = ROWBUF + (size_t)R * 8;          // CPW doubles

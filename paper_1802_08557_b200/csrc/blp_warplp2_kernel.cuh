@@ -23,8 +23,11 @@ template <int R, int S>
 struct Wl2Cfg {
     static constexpr int CPW = R + S;
     static constexpr int OPW = (CPW + 31) / 32;
-    static constexpr size_t TILE = 0;                              // S x 32 doubles
-    static constexpr size_t ROWBUF = TILE + (size_t)S * 32 * 8;    // R doubles
+    // column stride 33 doubles: a row read across columns (lane q -> tile[q][l],
+    // the pivot row's division) hits 16 distinct bank pairs instead of one
+    static constexpr int TS = 33;
+    static constexpr size_t TILE = 0;                              // S x TS doubles
+    static constexpr size_t ROWBUF = TILE + (size_t)S * TS * 8;    // R doubles
     static constexpr size_t RVEC = ROWBUF + (size_t)R * 8;         // CPW doubles
     static constexpr size_t CBV = RVEC + (size_t)((CPW + 1) & ~1) * 8;
     static constexpr size_t BYTES = CBV + 32 * 8;
@@ -74,7 +77,7 @@ __device__ __forceinline__ void wl2_candidates(const WlpDims &D, Wl2State<R, S> 
 template <int R, int S>
 __device__ __forceinline__ double wl2_at(const Wl2State<R, S> &St, const double *tile, int lane, int pos) {
     if (pos < R) return reg_pick<R>(St.a, pos);
-    return tile[(pos - R) * 32 + lane];
+    return tile[(pos - R) * Wl2Cfg<R, S>::TS + lane];
 }
 
 // pivot (tableau.py:218-244): av = this lane's entry of the entering column,
@@ -98,7 +101,7 @@ __device__ __forceinline__ void wl2_pivot(const WlpDims &D, Wl2State<R, S> &St, 
     for (int t = 0; t < Wl2State<R, S>::OPW; ++t) {
         const int pos = D.lane + 32 * t;
         if (pos < D.ncols) {
-            double *src = pos < R ? rowbuf + pos : tile + (pos - R) * 32 + l;
+            double *src = pos < R ? rowbuf + pos : tile + (pos - R) * C::TS + l;
             const double r = div_entry(*src, pe);
             rvec[pos] = r;
             if (pos >= R) *src = r;                              // row l of an smem column: final
@@ -131,9 +134,9 @@ __device__ __forceinline__ void wl2_pivot(const WlpDims &D, Wl2State<R, S> &St, 
 #pragma unroll
     for (int c = 0; c < S; c += 2) {
         const double2 r2 = reinterpret_cast<const double2 *>(rvec + R)[c / 2];
-        const double t0 = col[c * 32], t1 = col[(c + 1) * 32];
-        col[c * 32] = __dsub_rn(t0, __dmul_rn(fs, r2.x));
-        col[(c + 1) * 32] = __dsub_rn(t1, __dmul_rn(fs, r2.y));
+        const double t0 = col[c * C::TS], t1 = col[(c + 1) * C::TS];
+        col[c * C::TS] = __dsub_rn(t0, __dmul_rn(fs, r2.x));
+        col[(c + 1) * C::TS] = __dsub_rn(t1, __dmul_rn(fs, r2.y));
     }
 #pragma unroll
     for (int c = 0; c < R; c += 2) ld_shared_v2_if(mine, rv + 8u * c, St.a[c], St.a[c + 1]);
@@ -199,7 +202,7 @@ template <int R, int S>
 __device__ __forceinline__ double wl2_row_entry(unsigned char *smem, int row, int pos) {
     using C = Wl2Cfg<R, S>;
     return pos < R ? reinterpret_cast<const double *>(smem + C::ROWBUF)[pos]
-                   : reinterpret_cast<const double *>(smem + C::TILE)[(pos - R) * 32 + row];
+                   : reinterpret_cast<const double *>(smem + C::TILE)[(pos - R) * C::TS + row];
 }
 
 // _price_out (simplex.py:133-143), transposed: lane q rebuilds the reduced
@@ -334,7 +337,7 @@ warplp2_kernel(Batch B) {
                 if (j < n) { const double a = arow[j]; nonfinite |= !isfinite(a); v = __dmul_rn(a, sgn); }
                 else if (j < nvc) v = (j - n == D.lane) ? sgn : 0.0;
             }
-            tile[c * 32 + D.lane] = v;
+            tile[c * C::TS + D.lane] = v;
         }
         for (int j = D.lane; j < n; j += 32) nonfinite |= !isfinite(cg[j]);
         const bool invalid = __any_sync(kFull, nonfinite);
