@@ -1,16 +1,20 @@
-// blp_pairlp_kernel.cuh -- one 2-warp CTA per LP for 33..64 constraint rows
-// (the C4 support-function shape, 64 x 32 with 97 tableau columns).
+// blp_pairlp_kernel.cuh -- one CTA of NWR row-warps per LP: NWR = 2 for
+// 33..64 constraint rows (C4, the 64 x 32 support function: pairlp_*) and
+// NWR = 4 for 65..128 (C3, 100 x 100: quadlp_*).
 //
-// The warplp2 layout (blp_warplp2_kernel.cuh) stretched over two warps by
-// ROWS: warp w holds rows 32w..32w+31, lane L row 32w+L; a row's positions
-// [0, R) are registers, [R, R+S) live in the warp's column-major shared tile.
-// The transposed objective row is dealt to both warps in 32-position blocks
-// (position p -> warp (p/32)%2, lane p%32, slot p/64), so each lane divides
-// and prices at most two positions per pivot.  Per pivot three CTA barriers
-// (64 threads) separate: the per-warp leaving-row partials (A); the pivot
+// The warplp2 layout (blp_warplp2_kernel.cuh) stretched over NWR warps by
+// rows: thread r holds tableau row r; a row's positions [0, R) are
+// registers, [R, R+S) live in a column-major shared tile tile[c][row] with an
+// odd row stride ST >= m (conflict-free both along a column and along a row).
+// The transposed objective row is dealt to the warps in 32-position blocks
+// (position p -> warp (p/32)%NWR, lane p%32, slot p/(32 NWR)), so each lane
+// divides and prices at most OPW positions per pivot.  Per pivot three CTA
+// barriers separate: the per-warp leaving-row partials (A); the pivot
 // element, the old basic variable and the register half of the pivot row
 // published by the leaving row's lane (B); the pivot row r and the per-warp
-// entering candidates (C).  The row and column arithmetic is exactly the
+// entering candidates (C).  (Publishing every warp's candidate row before A
+// instead removes B but costs NWR x the row-transfer wavefronts: measured
+// slower, C4 17.5 -> 18.5 ms.)  The row and column arithmetic is exactly the
 // one-warp kernel's, so results are identical to it and to the reference.
 #pragma once
 
