@@ -181,13 +181,14 @@ bool use_pairlp(int m, int ncols, const char *name, Plan *p) {
 bool plan_pairlp(int m, int n, Plan *p) {
     const int ncols = n + m + 1;
     if (m > 64 && m <= 128) {
-        if (env_int("BLP_QUAD", 80) != 96 && use_pairlp<80, 122, 4, 101, 2>(m, ncols, "quadlp_r80_s122", p))
+        if (env_int("BLP_QUAD", 96) == 80 && use_pairlp<80, 122, 4, 101, 2>(m, ncols, "quadlp_r80_s122", p))
             return true;
         return use_pairlp<96, 106, 4, 129, 2>(m, ncols, "quadlp_r96_s106", p);
     }
     if (m <= 32 || m > 64) return false;
     if (env_int("BLP_PAIR", 62) == 50) return use_pairlp<50, 48, 2, 65, 7>(m, ncols, "pairlp_r50_s48", p);
-    return use_pairlp<62, 36, 2, 65, 6>(m, ncols, "pairlp_r62_s36", p);
+    if (use_pairlp<62, 36, 2, 65, 6>(m, ncols, "pairlp_r62_s36", p)) return true;      // C4: 97 columns
+    return use_pairlp<62, 48, 2, 65, 6>(m, ncols, "pairlp_r62_s48", p);                // up to 110 (50 x 50)
 }
 
 // BLP_KERNEL=warplp|pairlp|regtile|smem forces a family (testing / tuning).

@@ -213,9 +213,11 @@ __device__ __forceinline__ void pair_finish_pivot(const PairDims &D, PairState<R
         const double fs = mine ? 0.0 : av;  // row l of the smem columns already holds r
         pair_update_tile<R, S, ST>(tiles + D.row, rvec, fs);
     }
-    const unsigned rv = (unsigned)__cvta_generic_to_shared(rvec);
+    if ((l >> 5) == D.warp) {               // warp-uniform: only the leaving row's warp issues the reload
+        const unsigned rv = (unsigned)__cvta_generic_to_shared(rvec);
 #pragma unroll
-    for (int c = 0; c < R; c += 2) ld_shared_v2_if(mine, rv + 8u * c, St.a[c], St.a[c + 1]);
+        for (int c = 0; c < R; c += 2) ld_shared_v2_if(mine, rv + 8u * c, St.a[c], St.a[c + 1]);
+    }
 }
 
 // The leaving row's lane publishes pe, oldvar and its register half (before barrier B).
@@ -224,8 +226,10 @@ __device__ __forceinline__ void pair_publish_row(const PairDims &D, const PairSt
                                                  PairXch *X, int l, double av, bool with_pe) {
     const bool mine = D.row == l;
     const unsigned rb = (unsigned)__cvta_generic_to_shared(smem + PairCfg<R, S, NWR, ST>::ROWBUF);
+    if ((l >> 5) == D.warp) {               // warp-uniform: the other warps issue no (empty) stores
 #pragma unroll
-    for (int c = 0; c < R; c += 2) st_shared_v2_if(mine, rb + 8u * c, St.a[c], St.a[c + 1]);
+        for (int c = 0; c < R; c += 2) st_shared_v2_if(mine, rb + 8u * c, St.a[c], St.a[c + 1]);
+    }
     if (mine) {
         if (with_pe) X->pe = av;
         X->oldvar = St.basis_r;
@@ -311,8 +315,10 @@ __device__ __forceinline__ void pair_price_out(const PairDims &D, PairState<R, S
     for (int r = 0; r < D.m; ++r) {
         const double cb = cbv[r];
         if (cb == 0.0) continue;           // uniform across the CTA
+        if ((r >> 5) == D.warp) {
 #pragma unroll
-        for (int c = 0; c < R; c += 2) st_shared_v2_if(D.row == r, rb + 8u * c, St.a[c], St.a[c + 1]);
+            for (int c = 0; c < R; c += 2) st_shared_v2_if(D.row == r, rb + 8u * c, St.a[c], St.a[c + 1]);
+        }
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < PairState<R, S, NWR, ST>::OPW; ++t) {
