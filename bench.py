@@ -342,7 +342,7 @@ def main():
     # measured shared-memory bandwidth, BASELINE.md §2's roofline for C1-C4; the
     # register variants would only switch to the FP64 bound past 100% of it
     # (SURVEY.md §8d), so their FP64 fraction is reported alongside.
-    if variant.startswith(("warplp", "pairlp", "quadlp", "regtile", "smem")):
+    if variant.startswith(("warplp", "pairlp", "quadlp", "regtile", "smem", "cluster")):
         bound, unit, achieved, peak = "smem", "GB/s", achieved_gbs, smem_peak
         peak_src = "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
     else:

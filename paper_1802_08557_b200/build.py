@@ -17,14 +17,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libblp.so"
-SOURCES = [CSRC / "blp_capi.cu"]
-DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "blp.h"]
+SOURCES = [CSRC / "blp_capi.cu", CSRC / "blp_cluster.cu"]
+OBJDIR = PKG / "build"
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "blp.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-fmad=false",
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -45,8 +46,20 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", str(OUT), *map(str, SOURCES)]
-    subprocess.run(cmd, check=True)
+    # one object per translation unit, compiled in parallel, then one shared link
+    OBJDIR.mkdir(exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = OBJDIR / (src.stem + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+        procs.append((cmd, subprocess.Popen(cmd)))
+        objs.append(obj)
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-o", str(OUT), *map(str, objs)]
+    subprocess.run(link, check=True)
     return OUT
 
 

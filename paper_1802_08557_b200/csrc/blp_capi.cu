@@ -25,6 +25,7 @@
 #include "blp_tableau_kernel.cuh"
 #include "blp_box_kernel.cuh"
 #include "blp_cert_kernel.cuh"
+#include "blp_cluster.h"
 
 namespace {
 
@@ -54,6 +55,7 @@ struct Plan {
     int threads = 0;
     size_t smem = 0;
     long long slot = 0;  // doubles of global tableau per CTA (HBM-streamed variant)
+    bool cluster = false;  // cluster-resident variant (blp_cluster.cu): launched by blp_cluster::launch
 };
 
 int env_int(const char *name, int dflt) {
@@ -191,13 +193,31 @@ bool plan_pairlp(int m, int n, Plan *p) {
     return use_pairlp<62, 48, 2, 65, 6>(m, ncols, "pairlp_r62_s48", p);                // up to 110 (50 x 50)
 }
 
-// BLP_KERNEL=warplp|pairlp|regtile|smem forces a family (testing / tuning).
+// Cluster-resident variant: tableaux that no single-SM variant holds on chip
+// (the smem tableau exceeds 227 KB), up to 512 rows.
+bool plan_cluster(int m, int n, bool forced, Plan *p) {
+    if (!forced) {
+        if (env_int("BLP_FORCE_HBM", 0)) return false;
+        if (blp::make_tab_layout(m, n, 32, true).bytes <= kMaxDynSmem) return false;
+    }
+    if (!blp_cluster::shape_fits(m, n)) return false;
+    p->fn = nullptr;
+    p->name = blp_cluster::variant_name(m, n);
+    p->threads = 0;
+    p->smem = 0;
+    p->slot = 0;
+    p->cluster = true;
+    return true;
+}
+
+// BLP_KERNEL=warplp|pairlp|regtile|cluster|smem forces a family (testing / tuning).
 bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
     if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
     if ((any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p)) return true;
     if ((any || strcmp(force, "warplp") == 0 || strcmp(force, "regtile") == 0) && plan_regtile(m, n, p)) return true;
+    if ((any || strcmp(force, "cluster") == 0) && plan_cluster(m, n, !any, p)) return true;
     return plan_tableau(m, n, p);
 }
 
@@ -224,6 +244,32 @@ int device_sms(int dev, int *sms) {
     return BLP_OK;
 }
 
+void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c, long long count, int m, int n,
+                int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x, int32_t *it1,
+                int32_t *it2) {
+    B.A = A; B.b = b; B.c = c; B.count = count; B.m = m; B.n = n; B.shared_Ab = shared_Ab;
+    B.status = status; B.objective = objective; B.x = x; B.it1 = it1; B.it2 = it2;
+    B.next_lp = nullptr;
+    B.gtab = nullptr;
+    B.gtab_stride = 0;
+    B.lim.max_iterations = lim ? lim->max_iterations : 0;
+    B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
+    B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
+    B.lim.reserved = 0;
+}
+
+int launch_cluster(const double *A, const double *b, const double *c, long long count, int m, int n,
+                   int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
+                   int32_t *it1, int32_t *it2, cudaStream_t stream) {
+    blp::Batch B;
+    fill_batch(B, A, b, c, count, m, n, shared_Ab, lim, status, objective, x, it1, it2);
+    int K = 0, clusters = 0;
+    const cudaError_t e = blp_cluster::launch(B, stream, &K, &clusters);
+    if (e != cudaSuccess) return fail(BLP_ERR_CUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return BLP_OK;
+}
+
 int launch_solve(const double *A, const double *b, const double *c, long long count, int m, int n,
                  int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
                  int32_t *it1, int32_t *it2, cudaStream_t stream) {
@@ -235,6 +281,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     if (rc) return rc;
     Plan P;
     if (!plan_launch(m, n, &P)) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
+    if (P.cluster) return launch_cluster(A, b, c, count, m, n, shared_Ab, lim, status, objective, x, it1, it2, stream);
     BLP_CUDA_TRY(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     int occ = 0;
     BLP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, P.fn, P.threads, P.smem));

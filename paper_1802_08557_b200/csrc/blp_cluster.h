@@ -1,0 +1,25 @@
+// blp_cluster.h -- host side of the cluster-resident variant (blp_cluster.cu),
+// called by the C ABI's planner/launcher in blp_capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "blp_common.cuh"
+
+namespace blp_cluster {
+
+// Shape check without a device: some cluster size K <= 16 holds the tableau on
+// chip (one row per thread, m <= threads; the per-CTA tile within 227 KB).
+bool shape_fits(int m, int n);
+
+// Kernel name as reported by blp_kernel_variant.
+const char *variant_name(int m, int n);
+
+// Launch the persistent cluster grid (K chosen from the occupancy calculator:
+// the most SMs in use, then the smallest K).  K and the cluster count used are
+// returned for diagnostics.
+cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *clusters_used);
+
+}  // namespace blp_cluster

@@ -21,6 +21,7 @@ p.add_argument("--config", default="c2")
 p.add_argument("--count", type=int, default=None)
 p.add_argument("--steps", type=int, default=5)
 p.add_argument("--env", nargs="*", default=[""])
+p.add_argument("--max-iter", type=int, default=None, help="SolverLimits.max_iterations (per phase): isolates build cost")
 a = p.parse_args()
 A, b, c, shared, spec = bench.workload(a.config, a.count, 0)
 dev = torch.device("cuda:0")
@@ -38,7 +39,7 @@ for setting in a.env:
                x=torch.empty(cnt, n, dtype=torch.float64, device=dev),
                it1=torch.empty(cnt, dtype=torch.int32, device=dev),
                it2=torch.empty(cnt, dtype=torch.int32, device=dev))
-    lim = SolverLimits().to_native()
+    lim = SolverLimits(max_iterations=a.max_iter).to_native()
     _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared)
     torch.cuda.synchronize()
     ts = []

@@ -272,3 +272,28 @@ def test_general_form_batches_match_reference():
                 assert abs(got.objective[k] - w["objective"]) <= OBJ_RTOL * max(1.0, abs(w["objective"])), name
             checked += 1
     assert checked > 650
+
+
+CLUSTER_CASES = [((45, 30), 2), ((45, 30), 3), ((45, 30), 16), ((100, 150), 0), ((100, 150), 5),
+                 ((150, 150), 0), ((150, 150), 7), ((20, 400), 2), ((20, 400), 13), ((130, 90), 4),
+                 ((300, 200), 0)]
+
+
+@pytest.mark.parametrize("shape,K", CLUSTER_CASES)
+def test_cluster_kernel_matches_oracle(shape, K, monkeypatch):
+    """The cluster-resident variant (tableau split by columns over K CTAs, one DSMEM
+    exchange per pivot) forced on shapes either side of its register/tile split,
+    including K where a CTA owns fewer columns than its register half: equal to the oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, batch_solve_arrays, workloads
+    m, n = shape
+    cnt = 60 if m * n > 20000 else 150
+    A1, b1, c1 = workloads.afiro_arrays(cnt, seed=m * 1000 + n, m=m, n=n)
+    A2, b2, c2 = workloads.degenerate_arrays(cnt, seed=m * 1000 + n + 1, m=m, n=n)
+    A, b, c = (np.concatenate(v) for v in ((A1, A2), (b1, b2), (c1, c2)))
+    want = oracle.solve_batch(A, b, c)
+    monkeypatch.setenv("BLP_KERNEL", "cluster")
+    monkeypatch.setenv("BLP_CLUSTER_K", str(K))
+    assert _native.kernel_variant(m, n).startswith("cluster")
+    res = batch_solve_arrays(A, b, c)
+    compare(_native_dict(res), want, f"cluster {shape} K={K}")
