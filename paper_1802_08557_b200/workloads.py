@@ -147,7 +147,7 @@ def support_directions(count: int = 1_000_000, seed: int = 4, n: int = 32, offse
 
 
 def big_arrays(count: int = 10_000, seed: int = 5, dim: int = 500):
-    """C5: gen_random_lps(500, count, seed=5) packed (feasible start, HBM-streamed tableaux)."""
+    """C5: gen_random_lps(500, count, seed=5) packed (feasible start; 4 MB tableaux, beyond one SM)."""
     return random_arrays(dim, count, seed, True)
 
 
@@ -161,7 +161,7 @@ CONFIGS = {
     "c2": dict(m=28, n=32, count=100_000, doc="afiro-shaped 28x32 two-phase, mixed-sign b, seed 2"),
     "c3": dict(m=100, n=100, count=100_000, doc="100x100 degenerate mix + Bland, seed 3"),
     "c4": dict(m=64, n=32, count=1_000_000, doc="support function: one 64x32 polytope, 1e6 directions, seed 4"),
-    "c5": dict(m=500, n=500, count=10_000, doc="gen_random_lps(500, 1e4, seed=5), HBM-streamed"),
+    "c5": dict(m=500, n=500, count=10_000, doc="gen_random_lps(500, 1e4, seed=5), 4 MB tableaux (cluster-resident)"),
 }
 
 
