@@ -420,9 +420,14 @@ __device__ __forceinline__ void cl_pivot(ClCtx &X, double (&a)[RC], double &rhs,
 #pragma unroll
         for (int c = 0; c < RC; c += 2) cl_ld_v2_if(mine, rv + 8u * c, a[c], a[c + 1]);
     }
+#ifndef CL_ARRIVE_LATE
     if (pub) cl_arrive();
+#endif
     CL_PROF_MARK(6);
     if (X.live) cl_update_tile(smem_addr(X.tile + X.tid), smem_addr(S.rvec + RC), X.sc4, X.ld, mine ? 0.0 : f);
+#ifdef CL_ARRIVE_LATE
+    if (pub) cl_arrive();
+#endif
     if (KIND != kClRestore) obj = __dadd_rn(obj, __dmul_rn(rce, rrhs));   // tableau.py:242
     if (X.tid == 0) { S.basis[l] = e; S.isb[oldvar] = 0; S.isb[e] = 1; }
 }
