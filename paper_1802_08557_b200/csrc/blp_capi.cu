@@ -252,6 +252,8 @@ void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c
     B.next_lp = nullptr;
     B.gtab = nullptr;
     B.gtab_stride = 0;
+    B.defer_list = nullptr;
+    B.defer_count = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -264,9 +266,10 @@ int launch_cluster(const double *A, const double *b, const double *c, long long 
     blp::Batch B;
     fill_batch(B, A, b, c, count, m, n, shared_Ab, lim, status, objective, x, it1, it2);
     int K = 0, clusters = 0;
-    const cudaError_t e = blp_cluster::launch(B, stream, &K, &clusters);
+    const cudaError_t e = blp_cluster::lazy_enabled(m, n) ? blp_cluster::launch_lazy_then_cluster(B, stream)
+                                                           : blp_cluster::launch(B, stream, &K, &clusters);
     if (e != cudaSuccess) return fail(BLP_ERR_CUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    g_launches.fetch_add(blp_cluster::lazy_enabled(m, n) ? (shared_Ab ? 4 : 2) : 1, std::memory_order_relaxed);   // lazy, cluster (+ validate, finalize)
     return BLP_OK;
 }
 
@@ -300,6 +303,8 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.next_lp = reinterpret_cast<int *>(ws);
     B.gtab = P.slot ? reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256) : nullptr;
     B.gtab_stride = P.slot;
+    B.defer_list = nullptr;
+    B.defer_count = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;

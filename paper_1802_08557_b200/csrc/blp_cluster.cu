@@ -11,6 +11,7 @@
 
 #include "blp_cluster.h"
 #include "blp_cluster_kernel.cuh"
+#include "blp_lazy_kernel.cuh"
 
 namespace blp_cluster {
 namespace {
@@ -46,9 +47,12 @@ bool shape_fits(int m, int n) {
     return false;
 }
 
+bool lazy_enabled(int m, int n) {
+    return env_int("BLP_LAZY", 1) != 0 && blp::make_lazy_layout(m, n).bytes <= kMaxDynSmem;
+}
+
 const char *variant_name(int m, int n) {
-    (void)m; (void)n;
-    return "cluster_r32";
+    return lazy_enabled(m, n) ? "lazy+cluster_r32" : "cluster_r32";
 }
 
 cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *clusters_used) {
@@ -137,6 +141,65 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
         fprintf(stderr, "  total Gcyc=%.3f\n", tot / 1e9);
     }
 #endif
+    const cudaError_t ef = cudaFreeAsync(ws, stream);
+    return e != cudaSuccess ? e : ef;
+}
+
+cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
+    using LazyFn = void (*)(blp::Batch);
+    // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget)
+    const int nt = env_int("BLP_LAZY_NT", 256);
+    LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2> : (nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
+                                                                          : (LazyFn)blp::lazy_kernel<256, 4>);
+    const int threads = nt == 512 ? 512 : (nt == 128 ? 128 : 256);
+    const size_t smem = blp::make_lazy_layout(B.m, B.n).bytes;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, occ = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem)) != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const long long grid = std::min<long long>((long long)occ * sms, B.count);
+    const long long stride = blp::lazy_scratch_doubles(B.m, B.n);
+    // workspace: [0] LP queue, [64] deferred count | defer list | invalid flags | per-CTA replay history
+    const size_t list_bytes = ((size_t)B.count * sizeof(int) + 255) / 256 * 256;
+    const size_t flag_bytes = ((size_t)B.count + 255) / 256 * 256;
+    char *ws = nullptr;
+    e = cudaMallocAsync(reinterpret_cast<void **>(&ws), 256 + list_bytes + flag_bytes + (size_t)grid * stride * sizeof(double),
+                        stream);
+    if (e != cudaSuccess) return e;
+    unsigned char *flags = reinterpret_cast<unsigned char *>(ws + 256 + list_bytes);
+    e = cudaMemsetAsync(ws, 0, 256, stream);
+    blp::Batch Bl = B;
+    Bl.next_lp = reinterpret_cast<int *>(ws);
+    Bl.defer_count = reinterpret_cast<int *>(ws + 64);
+    Bl.defer_list = reinterpret_cast<int *>(ws + 256);
+    Bl.gtab = reinterpret_cast<double *>(ws + 256 + list_bytes + flag_bytes);
+    Bl.gtab_stride = stride;
+    if (e == cudaSuccess) {
+        fn<<<(unsigned)grid, threads, smem, stream>>>(Bl);
+        e = cudaGetLastError();
+    }
+    if (env_int("BLP_VERBOSE", 0))
+        fprintf(stderr, "blp lazy: m=%d n=%d grid=%lld x %d (%d per SM) smem=%zu scratch=%.1f MB\n", B.m, B.n, grid,
+                threads, occ, smem, grid * stride * 8.0 / 1e6);
+    if (e == cudaSuccess) {
+        blp::Batch Bc = B;                       // the dense kernel solves the deferred LPs
+        Bc.defer_list = Bl.defer_list;
+        Bc.defer_count = Bl.defer_count;
+        e = launch(Bc, stream, nullptr, nullptr);
+    }
+    if (e == cudaSuccess && B.shared_Ab && (long long)B.m * B.n > 0) {
+        // support mode: the shared polytope is validated once, then flagged LPs marked invalid
+        e = cudaMemsetAsync(flags, 0, flag_bytes, stream);
+        if (e == cudaSuccess) {
+            blp::lazy_validate_kernel<<<1, 256, 0, stream>>>(B.A, B.count, (long long)B.m * B.n, 1, flags);
+            blp::lazy_finalize_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((B.count + 255) / 256, 4LL * sms)),
+                                        256, 0, stream>>>(flags, B);
+            e = cudaGetLastError();
+        }
+    }
     const cudaError_t ef = cudaFreeAsync(ws, stream);
     return e != cudaSuccess ? e : ef;
 }

@@ -22,4 +22,12 @@ const char *variant_name(int m, int n);
 // returned for diagnostics.
 cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *clusters_used);
 
+// The lazy-tableau kernel (blp_lazy_kernel.cuh) over the whole batch, then the
+// cluster kernel over the LPs it deferred (phase 1 needed, or more than
+// kLazyMaxPivots pivots); both stream-ordered, no host synchronisation.
+cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream);
+
+// Whether the lazy path is used for this shape (BLP_LAZY=0 disables it).
+bool lazy_enabled(int m, int n);
+
 }  // namespace blp_cluster

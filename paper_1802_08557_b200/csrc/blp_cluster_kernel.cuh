@@ -636,9 +636,10 @@ cluster_kernel(Batch B) {
 #endif
     // LP queue: rank 0 claims LP t+1 while the cluster builds LP t and publishes it
     // (by LP parity) before the build's cluster barrier: one barrier per LP.
+    const long long count = batch_count(B);   // the deferred LPs when launched after the lazy kernel
     if (X.rank == 0 && X.tid == 0) S.nxt[0] = atomicAdd(B.next_lp, 1);
     cl_sync();
-    long long lp = cl_ld_s64(cl_map(smem_addr(&S.nxt[0]), 0u));
+    long long qi = cl_ld_s64(cl_map(smem_addr(&S.nxt[0]), 0u));
     double a[RC];
     // the staging buffer holds the next LP's first pass during a solve unless rank 0
     // needs it as x scratch (the tile alone is too small for x)
@@ -646,7 +647,8 @@ cluster_kernel(Batch B) {
     bool pre = false;
 
     for (int t = 0;; ++t) {
-        if (lp >= B.count) break;              // cluster-uniform
+        if (qi >= count) break;                // cluster-uniform
+        const long long lp = batch_lp(B, qi);
         CL_PROF_MARK(0);
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
@@ -744,7 +746,8 @@ cluster_kernel(Batch B) {
         int inv = 0;
         if (X.lane < X.K) inv = cl_ld_s32(cl_map(smem_addr(&S.inv[t & 1]), (unsigned)X.lane));
         const bool invalid = __any_sync(kFull, inv != 0);
-        const long long lpn = cl_ld_s64(cl_map(smem_addr(&S.nxt[(t + 1) & 1]), 0u));
+        const long long qn = cl_ld_s64(cl_map(smem_addr(&S.nxt[(t + 1) & 1]), 0u));
+        const long long lpn = qn < count ? batch_lp(B, qn) : B.count;
         // next LP: its first staging pass and b straight into shared memory (the staging
         // buffer is idle until then), the rest of its rows of this CTA's columns into L2
         pre = lpn < B.count && prefetch_stage;
@@ -819,7 +822,7 @@ cluster_kernel(Batch B) {
         }
         __syncthreads();
         CL_PROF_MARK(7);
-        lp = lpn;
+        qi = qn;
     }
     cl_sync();                                  // no CTA leaves while its shared memory may still be read
 #ifdef BLP_CL_PROF

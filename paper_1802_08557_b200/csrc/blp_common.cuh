@@ -60,7 +60,20 @@ struct Batch {
     double *gtab;          // global tableau slots (HBM-streamed variant), one per CTA
     long long gtab_stride; // doubles per slot
     Limits lim;
+    // Deferral (lazy kernel -> dense kernel): the lazy kernel appends the LPs it
+    // hands over to defer_list; a dense kernel launched with defer_list set solves
+    // exactly those (*defer_count of them, read on the device).
+    int *defer_list;
+    int *defer_count;
 };
+
+// Number of LPs a kernel launch processes, and the batch index of its k-th.
+__device__ __forceinline__ long long batch_count(const Batch &B) {
+    return B.defer_list ? (long long)*B.defer_count : B.count;
+}
+__device__ __forceinline__ long long batch_lp(const Batch &B, long long k) {
+    return B.defer_list ? (long long)B.defer_list[k] : k;
+}
 
 // np.argmax order: NaN first (lowest index among NaNs), then larger value,
 // then lower index.  kNone marks an empty slot.

@@ -1,0 +1,348 @@
+// blp_lazy_kernel.cuh -- exact LAZY tableau for large LPs that finish in few
+// pivots (C5: 500 x 500, ~14 pivots on a 501 x 1001 tableau).
+//
+// The dense algorithm (tableau.py:218-244) applies, at pivot t with leaving
+// row l_t, entering column e_t and pivot element pe_t,
+//     r^t_j = a_{l_t j} / pe_t                       (the new row l_t)
+//     a_ij <- a_ij - f^t_i * r^t_j   for i != l_t,   f^t_i = a_{i e_t} (before pivot t)
+// to every cell.  The algorithm, however, only ever READS the reduced-cost
+// row, the rhs column, the entering column and the pivot row.  So every other
+// cell can be left unevaluated: a cell's value after pivot k is recovered
+// exactly by replaying its own history,
+//     t0 = last pivot with l_{t0} = i (0 if none):  a = t0 ? r^{t0}_j : a^0_ij
+//     for t = t0+1 .. k:                           a = a - f^t_i * r^t_j
+// -- the very operations, operands and rounding order of the dense update, so
+// the value is bit-identical to what the dense tableau would hold.  This
+// kernel keeps the reduced-cost row, the rhs column and the basis dense (in
+// shared memory), stores the history vectors f^t (m) and r^t (n+m) in a
+// per-CTA global (L2-resident) scratch, and evaluates the entering column
+// (m cells) and the pivot row (n+m cells) by replay: O((n+m) k) work per pivot
+// instead of O(m (n+m)).
+//
+// Scope: single-phase LPs (b >= 0, so no artificials and every row sign is
+// +1) that finish within kLazyMaxPivots pivots.  An LP that needs phase 1 or
+// more pivots is appended to a deferral list and solved from scratch by the
+// dense cluster kernel launched right after on the same stream (identical
+// results either way).  Validation (model.py:263-301) still reads every
+// entry of A (streamed with 16-byte evict-first loads before the solve; the
+// CTAs resident on an SM drift apart, so one CTA's stream overlaps another's
+// latency-bound solve) -- C5 is bound by one HBM read of its inputs.  In
+// support mode (shared A) lazy_validate_kernel checks the polytope once.
+#pragma once
+
+#include "blp_common.cuh"
+#include "blp_keys.cuh"
+
+namespace blp {
+
+constexpr int kLazyMaxPivots = 64;
+
+struct LazyPart {
+    unsigned long long ckey[32];
+    int cidx[32], cbl[32];
+    unsigned long long lkey[32];
+    int lrow[32];
+    int flag[32];
+};
+
+struct LazyLayout {
+    size_t off_rhs, off_rc, off_fcur, off_basis, off_last, off_isb, off_part, off_misc;
+    size_t bytes;
+};
+
+__host__ __device__ inline LazyLayout make_lazy_layout(int m, int n) {
+    LazyLayout L;
+    const int nv = n + m, mm = m > 0 ? m : 1;
+    size_t o = 0;
+    auto al = [](size_t x) { return (x + 15) / 16 * 16; };
+    L.off_rhs = o;   o = al(o + (size_t)mm * 8);
+    L.off_rc = o;    o = al(o + (size_t)nv * 8);
+    L.off_fcur = o;  o = al(o + (size_t)mm * 8);
+    L.off_basis = o; o = al(o + (size_t)mm * 4);
+    L.off_last = o;  o = al(o + (size_t)mm * 4);
+    L.off_isb = o;   o = al(o + (size_t)nv);
+    L.off_part = o;  o = al(o + sizeof(LazyPart));
+    L.off_misc = o;  o = al(o + 64);
+    L.bytes = o;
+    return L;
+}
+
+// Scratch doubles per CTA: kLazyMaxPivots x (f^t: m, r^t: n+m).
+__host__ __device__ inline long long lazy_scratch_doubles(int m, int n) {
+    return (long long)kLazyMaxPivots * (2LL * m + n);
+}
+
+// Initial tableau cell a^0_ij of a single-phase LP (all row signs +1):
+// [A | I] (tableau.py:149-170).
+__device__ __forceinline__ double lazy_a0(const double *Ag, int n, int i, int j) {
+    return j < n ? Ag[(size_t)i * n + j] : ((j - n == i) ? 1.0 : 0.0);
+}
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+lazy_kernel(Batch B) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int m = B.m, n = B.n, nv = n + m;
+    const LazyLayout L = make_lazy_layout(m, n);
+    double *rhs = reinterpret_cast<double *>(smem + L.off_rhs);
+    double *rc = reinterpret_cast<double *>(smem + L.off_rc);
+    double *fcur = reinterpret_cast<double *>(smem + L.off_fcur);
+    int *basis = reinterpret_cast<int *>(smem + L.off_basis);
+    int *lastpiv = reinterpret_cast<int *>(smem + L.off_last);     // 1-based pivot number, 0 = never
+    unsigned char *isb = smem + L.off_isb;
+    LazyPart *P = reinterpret_cast<LazyPart *>(smem + L.off_part);
+    long long *s_lp = reinterpret_cast<long long *>(smem + L.off_misc);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
+    // history: F[t] (m doubles), R[t] (nv doubles), t = 0 .. kLazyMaxPivots-1 (pivot t+1)
+    double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)B.gtab_stride;
+    double *Rh = Fh + (size_t)kLazyMaxPivots * m;
+    const int max_iter = B.lim.max_iterations > 0 ? B.lim.max_iterations : 50 * (m + n);
+    const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
+    const unsigned long long kSent = key_max(kSentinel), kDeg = key_max(kDegenerateTol), kTolK = key_max(kTol);
+
+    for (;;) {
+        if (tid == 0) *s_lp = atomicAdd(B.next_lp, 1);
+        __syncthreads();
+        const long long lp = *s_lp;
+        if (lp >= B.count) break;
+        const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
+        const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
+        const double *cg = B.c + (size_t)lp * n;
+
+        // ---- b: phase 1 needed? (then the dense kernel takes the LP) ----
+        bool nonfinite = false, neg = false;
+        for (int i = tid; i < m; i += NT) {
+            const double bi = bg[i];
+            nonfinite |= !isfinite(bi);
+            neg |= bi < 0.0;
+            rhs[i] = bi;                      // b * (+1)
+            basis[i] = n + i;
+            lastpiv[i] = 0;
+        }
+        if (__syncthreads_or(neg)) {
+            if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
+            __syncthreads();
+            continue;
+        }
+        // ---- validate (model.py:263-301): every entry of A, streamed once; b above, c below ----
+        if (!B.shared_Ab) {
+            const size_t total = (size_t)m * n;
+            const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;   // 16-byte align the body
+            if (tid == 0 && head && total) nonfinite |= !isfinite(Ag[0]);
+            const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
+            const size_t n2 = (total - head) / 2;
+            size_t q = tid;
+            for (; q + 3 * NT < n2; q += 4 * NT) {
+                const double2 v0 = __ldcs(A2 + q), v1 = __ldcs(A2 + q + NT), v2 = __ldcs(A2 + q + 2 * NT),
+                              v3 = __ldcs(A2 + q + 3 * NT);
+                nonfinite |= !(isfinite(v0.x) && isfinite(v0.y) && isfinite(v1.x) && isfinite(v1.y) &&
+                               isfinite(v2.x) && isfinite(v2.y) && isfinite(v3.x) && isfinite(v3.y));
+            }
+            for (; q < n2; q += NT) {
+                const double2 v = __ldcs(A2 + q);
+                nonfinite |= !(isfinite(v.x) && isfinite(v.y));
+            }
+            if (tid == 0 && ((total - head) & 1)) nonfinite |= !isfinite(Ag[total - 1]);
+        }
+        for (int j = tid; j < nv; j += NT) {
+            const double cj = j < n ? cg[j] : 0.0;
+            nonfinite |= !isfinite(cj);
+            rc[j] = cj;                         // phase 2 runs on c directly (simplex.py:168,180)
+            isb[j] = j >= n ? 1 : 0;            // slacks basic
+        }
+        const bool invalid = __syncthreads_or(nonfinite);
+
+        int8_t status = kOptimal;
+        int iters = 0;
+        double obj = 0.0;
+        bool deferred = false;
+        if (invalid) {
+            status = kInvalid;
+        } else {
+            // initial entering candidates
+            {
+                unsigned long long ck = kKeyEmptyMax;
+                int ci = kNone, cb = kNone;
+                for (int j = tid; j < nv; j += NT) {
+                    if (isb[j]) continue;
+                    const unsigned long long k = key_max(rc[j]);
+                    if (k > ck || (k == ck && j < ci)) { ck = k; ci = j; }
+                    if (rc[j] > kTol && j < cb) cb = j;
+                }
+                const unsigned long long kw = warp_max_key(ck);
+                const int iw = warp_index_of(ck, kw, ci);
+                const int bw = warp_min_int(cb);
+                if (lane == 0) { P->ckey[warp] = kw; P->cidx[warp] = iw; P->cbl[warp] = bw; }
+            }
+            __syncthreads();
+            int degenerate_run = 0;
+            bool use_bland = false;
+            int prev_l = -1, prev_e = -1, prev_old = -1;
+            // _run_phase (simplex.py:63-91)
+            for (int k = 0;; ++k) {                   // pivot number k+1; history slot k
+                // previous pivot's bookkeeping (after the barrier that ended it)
+                if (prev_l >= 0) {
+                    if (tid == 0) { basis[prev_l] = prev_e; isb[prev_old] = 0; isb[prev_e] = 1; }
+                    if (tid == (prev_l % NT)) lastpiv[prev_l] = k;
+                }
+                if (k == max_iter) { status = kIterationLimit; iters = max_iter; break; }
+                // choose_entering[_bland] from the warp partials
+                int e;
+                {
+                    unsigned long long kk = lane < NW ? P->ckey[lane] : kKeyEmptyMax;
+                    const int ii = lane < NW ? P->cidx[lane] : kNone, bb = lane < NW ? P->cbl[lane] : kNone;
+                    const unsigned long long kw = warp_max_key(kk);
+                    const int ew = warp_index_of(kk, kw, ii);
+                    const int bw = warp_min_int(bb);
+                    if (use_bland) e = bw == kNone ? -1 : bw;
+                    else e = (ew == kNone || kw <= kTolK) ? -1 : ew;
+                }
+                if (e < 0) { iters = k; break; }   // optimal
+                if (k == kLazyMaxPivots) { deferred = true; break; }
+                const double rce = rc[e];
+                // entering column by replay (f_i = a_ie before this pivot); ratio test
+                unsigned long long lk = kKeyEmptyMin;
+                int li = kNone;
+                const double *Rcol = Rh + e;
+                for (int i = tid; i < m; i += NT) {
+                    const int t0 = lastpiv[i];
+                    double a = t0 ? Rcol[(size_t)(t0 - 1) * nv] : lazy_a0(Ag, n, i, e);
+                    for (int t = t0; t < k; ++t) a = __dsub_rn(a, __dmul_rn(Fh[(size_t)t * m + i], Rcol[(size_t)t * nv]));
+                    fcur[i] = a;
+                    Fh[(size_t)k * m + i] = a;
+                    const unsigned long long key = key_min(ratio_entry(rhs[i], a));
+                    if (key < lk) { lk = key; li = i; }     // rows ascend per thread
+                }
+                {
+                    const unsigned long long kw = warp_min_key(lk);
+                    const int lw = warp_index_of(lk, kw, li);
+                    if (lane == 0) { P->lkey[warp] = kw; P->lrow[warp] = lw; }
+                }
+                __syncthreads();  // S1
+                unsigned long long kmin;
+                int l;
+                {
+                    const unsigned long long kk = lane < NW ? P->lkey[lane] : kKeyEmptyMin;
+                    const int rr = lane < NW ? P->lrow[lane] : kNone;
+                    kmin = warp_min_key(kk);
+                    l = warp_index_of(kk, kmin, rr);
+                }
+                if (l == kNone || kmin >= kSent) { status = kUnbounded; iters = k; break; }
+                if (kmin != 0ull && kmin <= kDeg) {                 // simplex.py:84-90
+                    ++degenerate_run;
+                    if (B.lim.anti_cycling && degenerate_run >= trigger) use_bland = true;
+                } else {
+                    degenerate_run = 0;
+                    use_bland = false;
+                }
+                const double pe = fcur[l];
+                const double rrhs = div_entry(rhs[l], pe);
+                const int oldvar = basis[l];
+                const int t0l = lastpiv[l];
+                // pivot row by replay, divided by pe; objective row; next candidates
+                unsigned long long ck = kKeyEmptyMax;
+                int ci = kNone, cb = kNone;
+                double *Rk = Rh + (size_t)k * nv;
+                for (int j = tid; j < nv; j += NT) {
+                    double a = t0l ? Rh[(size_t)(t0l - 1) * nv + j] : lazy_a0(Ag, n, l, j);
+                    for (int t = t0l; t < k; ++t) a = __dsub_rn(a, __dmul_rn(Fh[(size_t)t * m + l], Rh[(size_t)t * nv + j]));
+                    const double r = div_entry(a, pe);
+                    Rk[j] = r;
+                    const double v = __dsub_rn(rc[j], __dmul_rn(rce, r));
+                    rc[j] = v;
+                    if (!((j == e) || (j != oldvar && isb[j]))) {
+                        const unsigned long long kv = key_max(v);
+                        if (kv > ck || (kv == ck && j < ci)) { ck = kv; ci = j; }
+                        if (v > kTol && j < cb) cb = j;
+                    }
+                }
+                {
+                    const unsigned long long kw = warp_max_key(ck);
+                    const int iw = warp_index_of(ck, kw, ci);
+                    const int bw = warp_min_int(cb);
+                    if (lane == 0) { P->ckey[warp] = kw; P->cidx[warp] = iw; P->cbl[warp] = bw; }
+                }
+                for (int i = tid; i < m; i += NT) rhs[i] = i == l ? rrhs : __dsub_rn(rhs[i], __dmul_rn(fcur[i], rrhs));
+                obj = __dadd_rn(obj, __dmul_rn(rce, rrhs));          // tableau.py:242
+                prev_l = l; prev_e = e; prev_old = oldvar;
+                __syncthreads();  // S3
+            }
+            __syncthreads();
+            if (prev_l >= 0 && tid == 0) { basis[prev_l] = prev_e; }
+            __syncthreads();
+        }
+        (void)obj;
+        if (deferred) {
+            if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
+            __syncthreads();
+            continue;
+        }
+        // ---- _extract_point (simplex.py:146-151) and c @ x ----
+        double *xs = fcur;                       // reuse: n <= ? -> write x straight to global
+        (void)xs;
+        double *xg = B.x + (size_t)lp * n;
+        for (int j = tid; j < n; j += NT) xg[j] = 0.0;
+        __syncthreads();
+        if (status == kOptimal)
+            for (int i = tid; i < m; i += NT)
+                if (basis[i] < n) xg[basis[i]] = rhs[i];
+        __syncthreads();
+        if (warp == 0) {
+            double s = 0.0;
+            if (status == kOptimal) {
+                for (int j = lane; j < n; j += 32) s = __dadd_rn(s, __dmul_rn(cg[j], xg[j]));
+#pragma unroll
+                for (int off = 16; off; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(kFull, s, off));
+            }
+            if (lane == 0) {
+                B.objective[lp] = status == kOptimal ? s : __longlong_as_double(0x7ff8000000000000LL);
+                B.status[lp] = status;
+                B.it1[lp] = 0;
+                B.it2[lp] = iters;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Finiteness of every entry of A (model.py:263-301), streamed once with
+// 16-byte loads; flag[lp] = 1 for an LP holding a non-finite entry.  A shared
+// polytope (support mode) is scanned once and flags every LP.
+__global__ void __launch_bounds__(256)
+lazy_validate_kernel(const double *A, long long count, long long per_lp, int shared_Ab, unsigned char *flag) {
+    const long long total = shared_Ab ? per_lp : count * per_lp;
+    const long long n2 = total / 2;                 // A is 256-byte aligned (cudaMalloc / torch)
+    const double2 *A2 = reinterpret_cast<const double2 *>(A);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += stride) {
+        const double2 v = __ldcs(A2 + q);
+        if (!isfinite(v.x) || !isfinite(v.y)) {
+            if (shared_Ab) { for (long long k = 0; k < count; ++k) flag[k] = 1; }
+            else {
+                if (!isfinite(v.x)) flag[(2 * q) / per_lp] = 1;
+                if (!isfinite(v.y)) flag[(2 * q + 1) / per_lp] = 1;
+            }
+        }
+    }
+    if ((total & 1) && blockIdx.x == 0 && threadIdx.x == 0 && !isfinite(A[total - 1])) {
+        if (shared_Ab) { for (long long k = 0; k < count; ++k) flag[k] = 1; }
+        else flag[(total - 1) / per_lp] = 1;
+    }
+}
+
+// Outputs of the LPs lazy_validate_kernel flagged: BLP_STATUS_INVALID, as the
+// dense kernels report them (the host then raises validate()'s ValueError).
+__global__ void lazy_finalize_kernel(const unsigned char *flag, Batch B) {
+    for (long long lp = (long long)blockIdx.x * blockDim.x + threadIdx.x; lp < B.count;
+         lp += (long long)gridDim.x * blockDim.x) {
+        if (!flag[lp]) continue;
+        B.status[lp] = kInvalid;
+        B.objective[lp] = __longlong_as_double(0x7ff8000000000000LL);
+        B.it1[lp] = 0;
+        B.it2[lp] = 0;
+        for (int j = 0; j < B.n; ++j) B.x[(size_t)lp * B.n + j] = 0.0;
+    }
+}
+
+}  // namespace blp

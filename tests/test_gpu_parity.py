@@ -294,6 +294,77 @@ def test_cluster_kernel_matches_oracle(shape, K, monkeypatch):
     want = oracle.solve_batch(A, b, c)
     monkeypatch.setenv("BLP_KERNEL", "cluster")
     monkeypatch.setenv("BLP_CLUSTER_K", str(K))
+    monkeypatch.setenv("BLP_LAZY", "0")          # the dense cluster kernel for every LP
     assert _native.kernel_variant(m, n).startswith("cluster")
     res = batch_solve_arrays(A, b, c)
     compare(_native_dict(res), want, f"cluster {shape} K={K}")
+
+
+LAZY_CASES = [(150, 150), (300, 200), (100, 150), (40, 300)]   # 500 x 500: the c5 goldens
+
+
+def _single_phase_mix(m, n, seed):
+    """Single-phase LPs (b >= 0): the C5 recipe, plus the degenerate/unbounded C3 recipe
+    with |b| (zero rows of b make ties and Bland switches), plus long-running afiro-style
+    LPs with |b| that exceed the lazy kernel's pivot budget and must be deferred."""
+    from paper_1802_08557_b200 import workloads
+    cnt = 24 if m * n > 100_000 else 80
+    A1, b1, c1 = workloads.random_arrays(max(m, n), cnt, seed)
+    A1, b1, c1 = A1[:, :m, :n].copy(), b1[:, :m].copy(), c1[:, :n].copy()
+    A2, b2, c2 = workloads.degenerate_arrays(cnt, seed=seed + 1, m=m, n=n)
+    A3, b3, c3 = workloads.afiro_arrays(cnt // 2, seed=seed + 2, m=m, n=n)
+    A = np.concatenate([A1, A2, A3])
+    b = np.abs(np.concatenate([b1, b2, b3]))
+    c = np.concatenate([c1, c2, c3])
+    return A, b, c
+
+
+@pytest.mark.parametrize("m,n", LAZY_CASES)
+def test_lazy_tableau_matches_oracle(m, n, monkeypatch):
+    """The exact lazy-tableau kernel (entering column and pivot row evaluated by replaying
+    the rank-1 update history) on single-phase LPs, with the cluster kernel taking the
+    LPs it defers (phase 1 needed / more than 64 pivots): equal to the oracle, including
+    iteration limits hit inside the lazy kernel."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import SolverLimits, _native, batch_solve_arrays
+    A, b, c = _single_phase_mix(m, n, seed=m * 7 + n)
+    monkeypatch.setenv("BLP_KERNEL", "cluster")
+    assert _native.kernel_variant(m, n).startswith("lazy")
+    want = oracle.solve_batch(A, b, c)
+    assert ((want["it1"] + want["it2"]) > 64).any() or m * n > 100_000
+    compare(_native_dict(batch_solve_arrays(A, b, c)), want, f"lazy {m}x{n}")
+    for mi in (1, 5, 40):
+        want = oracle.solve_batch(A, b, c, max_iterations=mi)
+        got = batch_solve_arrays(A, b, c, SolverLimits(max_iterations=mi))
+        compare(_native_dict(got), want, f"lazy {m}x{n} max_iterations={mi}")
+
+
+def test_lazy_disabled_matches_lazy(monkeypatch):
+    """BLP_LAZY=0 (dense cluster kernel for everything) gives the same bits."""
+    from paper_1802_08557_b200 import batch_solve_arrays
+    A, b, c = _single_phase_mix(150, 150, seed=5)
+    r1 = _native_dict(batch_solve_arrays(A, b, c))
+    monkeypatch.setenv("BLP_LAZY", "0")
+    r2 = _native_dict(batch_solve_arrays(A, b, c))
+    for k in r1:
+        assert np.array_equal(r1[k], r2[k], equal_nan=True), k
+
+
+def test_lazy_path_flags_non_finite_entries():
+    """A non-finite entry anywhere in A (found by the concurrent validation pass), b or c
+    of a lazy-path batch: that LP comes back BLP_STATUS_INVALID, the others solved."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, workloads
+    A, b, c = workloads.random_arrays(150, 12, seed=9)
+    A[3, 149, 148] = np.nan
+    A[5, 0, 0] = np.inf
+    b[7, 10] = np.nan
+    c[9, 149] = -np.inf
+    assert _native.kernel_variant(150, 150).startswith("lazy")
+    got = _native.solve_host(A, b, c, _native.make_limits())
+    bad = [3, 5, 7, 9]
+    assert (got["status"][bad] == 5).all()
+    ok = [k for k in range(12) if k not in bad]
+    want = oracle.solve_batch(A[ok], b[ok], c[ok])
+    for key in ("status", "it1", "it2", "x"):
+        assert np.array_equal(got[key][ok], want[key]), key
