@@ -368,3 +368,21 @@ def test_lazy_path_flags_non_finite_entries():
     want = oracle.solve_batch(A[ok], b[ok], c[ok])
     for key in ("status", "it1", "it2", "x"):
         assert np.array_equal(got[key][ok], want[key]), key
+
+
+def test_lazy_support_mode_matches_oracle():
+    """Support-function mode (one polytope, many objective directions) on a lazy-path
+    shape, plus a non-finite polytope entry flagging every direction invalid."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, support_batch, workloads
+    A, b, c = workloads.random_arrays(150, 1, seed=21)
+    A, b = A[0], b[0]
+    C = np.random.default_rng(22).normal(size=(300, 150))
+    assert _native.kernel_variant(150, 150).startswith("lazy")
+    got = support_batch(A, b, C)
+    want = oracle.solve_batch(A, b, C, shared_Ab=True)
+    compare(_native_dict(got), want, "lazy support 150x150")
+    A2 = A.copy()
+    A2[77, 3] = np.nan
+    res = _native.solve_host(A2, b, C, _native.make_limits(), shared_Ab=True)
+    assert (res["status"] == 5).all()
