@@ -55,6 +55,7 @@ struct Plan {
     int threads = 0;
     size_t smem = 0;
     long long slot = 0;  // doubles of global tableau per CTA (HBM-streamed variant)
+    bool lazy = false;     // the exact lazy-tableau kernel runs first; this one takes its deferred LPs
     bool cluster = false;  // cluster-resident variant (blp_cluster.cu): launched by blp_cluster::launch
 };
 
@@ -111,6 +112,8 @@ bool plan_tableau(int m, int n, Plan *p) {
     else if (rpl <= 16) { p->fn = blp::tableau_kernel<16, false, 512>; p->name = "hbm_rpl16"; maxt = 512; }
     else if (rpl <= 32) { p->fn = blp::tableau_kernel<32, false, 256>; p->name = "hbm_rpl32"; maxt = 256; }
     else return false;
+    // HBM-streamed shapes: the exact lazy tableau first, this kernel for what it defers
+    p->lazy = !smem_tab && env_int("BLP_FORCE_HBM", 0) == 0 && blp_cluster::lazy_enabled(m, n);
     // threads: resident CTAs of one SM hold ~32 warps (register budget ~64/thread),
     // never more warps than columns
     const int ncols = n + m + 1;
@@ -123,6 +126,11 @@ bool plan_tableau(int m, int n, Plan *p) {
     const blp::TabLayout L = blp::make_tab_layout(m, n, p->threads / 32, smem_tab);
     p->smem = L.bytes;
     p->slot = smem_tab ? 0 : (long long)L.ncols * L.ld;
+    if (p->lazy) {
+        static thread_local std::string name;
+        name = std::string("lazy+") + p->name;
+        p->name = name.c_str();
+    }
     return true;
 }
 
@@ -260,6 +268,13 @@ void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c
     B.lim.reserved = 0;
 }
 
+blp::Batch Bproto(const double *A, const double *b, const double *c, long long count, int m, int n, int shared_Ab,
+                  const blp_limits *lim, int8_t *status, double *objective, double *x, int32_t *it1, int32_t *it2) {
+    blp::Batch B;
+    fill_batch(B, A, b, c, count, m, n, shared_Ab, lim, status, objective, x, it1, it2);
+    return B;
+}
+
 int launch_cluster(const double *A, const double *b, const double *c, long long count, int m, int n,
                    int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
                    int32_t *it1, int32_t *it2, cudaStream_t stream) {
@@ -291,6 +306,14 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     if (occ < 1) return fail(BLP_ERR_TOO_LARGE, "kernel variant cannot be resident on an SM");
     long long grid = (long long)occ * sms;
     if (grid > count) grid = count;
+    int *defer_list = nullptr, *defer_count = nullptr;
+    void *lazy_ws = nullptr;
+    if (P.lazy) {   // the lazy kernel over the batch; this kernel then solves only what it defers
+        const cudaError_t le = blp_cluster::launch_lazy(Bproto(A, b, c, count, m, n, shared_Ab, lim, status, objective,
+                                                               x, it1, it2), stream, &defer_list, &defer_count, &lazy_ws);
+        if (le != cudaSuccess) return fail(BLP_ERR_CUDA, std::string("lazy launch: ") + cudaGetErrorString(le));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
 
     const size_t ws_bytes = 256 + (size_t)P.slot * sizeof(double) * (size_t)grid;
     void *ws = nullptr;
@@ -303,8 +326,8 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.next_lp = reinterpret_cast<int *>(ws);
     B.gtab = P.slot ? reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256) : nullptr;
     B.gtab_stride = P.slot;
-    B.defer_list = nullptr;
-    B.defer_count = nullptr;
+    B.defer_list = defer_list;
+    B.defer_count = defer_count;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -314,6 +337,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     g_launches.fetch_add(1, std::memory_order_relaxed);
     BLP_CUDA_TRY(cudaGetLastError());
     BLP_CUDA_TRY(cudaFreeAsync(ws, stream));
+    if (P.lazy) BLP_CUDA_TRY(blp_cluster::finish_lazy(B, stream, lazy_ws));
     return BLP_OK;
 }
 

@@ -145,14 +145,16 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
     return e != cudaSuccess ? e : ef;
 }
 
-cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
+cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_list, int **defer_count, void **ws_out) {
     using LazyFn = void (*)(blp::Batch);
-    // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget)
+    // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget;
+    // C5 1e4: 256 -> 6.73 ms, 512 -> 6.96, 128 -> 7.71)
     const int nt = env_int("BLP_LAZY_NT", 256);
     LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2> : (nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
                                                                           : (LazyFn)blp::lazy_kernel<256, 4>);
     const int threads = nt == 512 ? 512 : (nt == 128 ? 128 : 256);
     const size_t smem = blp::make_lazy_layout(B.m, B.n).bytes;
+    *ws_out = nullptr;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, occ = 0;
@@ -169,6 +171,7 @@ cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
     e = cudaMallocAsync(reinterpret_cast<void **>(&ws), 256 + list_bytes + flag_bytes + (size_t)grid * stride * sizeof(double),
                         stream);
     if (e != cudaSuccess) return e;
+    *ws_out = ws;
     unsigned char *flags = reinterpret_cast<unsigned char *>(ws + 256 + list_bytes);
     e = cudaMemsetAsync(ws, 0, 256, stream);
     blp::Batch Bl = B;
@@ -177,6 +180,8 @@ cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
     Bl.defer_list = reinterpret_cast<int *>(ws + 256);
     Bl.gtab = reinterpret_cast<double *>(ws + 256 + list_bytes + flag_bytes);
     Bl.gtab_stride = stride;
+    *defer_list = Bl.defer_list;
+    *defer_count = Bl.defer_count;
     if (e == cudaSuccess) {
         fn<<<(unsigned)grid, threads, smem, stream>>>(Bl);
         e = cudaGetLastError();
@@ -184,23 +189,46 @@ cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
     if (env_int("BLP_VERBOSE", 0))
         fprintf(stderr, "blp lazy: m=%d n=%d grid=%lld x %d (%d per SM) smem=%zu scratch=%.1f MB\n", B.m, B.n, grid,
                 threads, occ, smem, grid * stride * 8.0 / 1e6);
+    if (e == cudaSuccess && B.shared_Ab && (long long)B.m * B.n > 0) {
+        // support mode: the shared polytope is validated once by finish_lazy, after the
+        // dense launch (its flags start cleared here)
+        e = cudaMemsetAsync(flags, 0, flag_bytes, stream);
+    }
+    return e;
+}
+
+// Support mode only: after the dense kernel, mark every LP invalid if the shared
+// polytope holds a non-finite entry (the lazy kernel does not scan A then).
+static cudaError_t launch_lazy_finalize(const blp::Batch &B, cudaStream_t stream, void *ws) {
+    if (!B.shared_Ab || (long long)B.m * B.n == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t list_bytes = ((size_t)B.count * sizeof(int) + 255) / 256 * 256;
+    unsigned char *flags = reinterpret_cast<unsigned char *>(static_cast<char *>(ws) + 256 + list_bytes);
+    blp::lazy_validate_kernel<<<1, 256, 0, stream>>>(B.A, B.count, (long long)B.m * B.n, 1, flags);
+    blp::lazy_finalize_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((B.count + 255) / 256, 4LL * sms)),
+                                256, 0, stream>>>(flags, B);
+    return cudaGetLastError();
+}
+
+cudaError_t finish_lazy(const blp::Batch &B, cudaStream_t stream, void *ws) {
+    cudaError_t e = launch_lazy_finalize(B, stream, ws);
+    const cudaError_t ef = ws ? cudaFreeAsync(ws, stream) : cudaSuccess;
+    return e != cudaSuccess ? e : ef;
+}
+
+cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
+    int *dl = nullptr, *dc = nullptr;
+    void *ws = nullptr;
+    cudaError_t e = launch_lazy(B, stream, &dl, &dc, &ws);
     if (e == cudaSuccess) {
         blp::Batch Bc = B;                       // the dense kernel solves the deferred LPs
-        Bc.defer_list = Bl.defer_list;
-        Bc.defer_count = Bl.defer_count;
+        Bc.defer_list = dl;
+        Bc.defer_count = dc;
         e = launch(Bc, stream, nullptr, nullptr);
     }
-    if (e == cudaSuccess && B.shared_Ab && (long long)B.m * B.n > 0) {
-        // support mode: the shared polytope is validated once, then flagged LPs marked invalid
-        e = cudaMemsetAsync(flags, 0, flag_bytes, stream);
-        if (e == cudaSuccess) {
-            blp::lazy_validate_kernel<<<1, 256, 0, stream>>>(B.A, B.count, (long long)B.m * B.n, 1, flags);
-            blp::lazy_finalize_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((B.count + 255) / 256, 4LL * sms)),
-                                        256, 0, stream>>>(flags, B);
-            e = cudaGetLastError();
-        }
-    }
-    const cudaError_t ef = cudaFreeAsync(ws, stream);
+    const cudaError_t ef = finish_lazy(B, stream, ws);
     return e != cudaSuccess ? e : ef;
 }
 

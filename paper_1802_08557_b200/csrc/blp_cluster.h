@@ -30,4 +30,13 @@ cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream);
 // Whether the lazy path is used for this shape (BLP_LAZY=0 disables it).
 bool lazy_enabled(int m, int n);
 
+// The lazy kernel alone: on return *defer_list / *defer_count (device) name the
+// LPs a dense kernel must still solve; *ws is the workspace to cudaFreeAsync
+// after that dense launch.
+cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_list, int **defer_count, void **ws);
+
+// After the dense launch: support-mode validation of the shared polytope, then
+// the workspace is released (stream-ordered).
+cudaError_t finish_lazy(const blp::Batch &B, cudaStream_t stream, void *ws);
+
 }  // namespace blp_cluster

@@ -401,8 +401,9 @@ tableau_kernel(Batch B) {
     for (;;) {
         if (X.tid == 0) { X.misc[0] = atomicAdd(B.next_lp, 1); X.misc[1] = 0; }
         __syncthreads();
-        const long long lp = X.misc[0];
-        if (lp >= B.count) break;
+        const long long qi = X.misc[0];
+        if (qi >= batch_count(B)) break;      // the deferred LPs when launched after the lazy kernel
+        const long long lp = batch_lp(B, qi);
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;

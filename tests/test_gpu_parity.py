@@ -386,3 +386,17 @@ def test_lazy_support_mode_matches_oracle():
     A2[77, 3] = np.nan
     res = _native.solve_host(A2, b, C, _native.make_limits(), shared_Ab=True)
     assert (res["status"] == 5).all()
+
+
+def test_lazy_ahead_of_hbm_kernel():
+    """Beyond the cluster kernel's rows (m > 512) the lazy tableau runs ahead of the
+    HBM-streamed kernel, which solves what it defers (here: phase-1 LPs)."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, batch_solve_arrays, workloads
+    A, b, c = workloads.random_arrays(600, 10, seed=31)
+    A2, b2, c2 = workloads.random_arrays(600, 3, seed=32, feasible_start=False)   # b < 0: phase 1, infeasible
+    A, b, c = np.concatenate([A, A2]), np.concatenate([b, b2]), np.concatenate([c, c2])
+    assert _native.kernel_variant(600, 600).startswith("lazy+hbm")
+    got = batch_solve_arrays(A, b, c)
+    compare(_native_dict(got), oracle.solve_batch(A, b, c), "lazy+hbm 600x600")
+    assert (got.status[-3:] == 2).all()
