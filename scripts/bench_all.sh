@@ -3,9 +3,9 @@
 mkdir -p gpurun_out
 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 python bench.py --config c1 --no-cpu-baseline --steps 50 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-python bench.py --config c3 --count 20000 --no-cpu-baseline --steps 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+python bench.py --config c3 --no-cpu-baseline --steps 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
 python bench.py --config c4 --no-cpu-baseline --steps 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-python bench.py --config c5 --count 2000 --no-cpu-baseline --steps 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+python bench.py --config c5 --no-cpu-baseline --steps 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 for c in c1 c2 c3 c4 c5; do python - "$c" <<'PY'
 import json, sys
 c = sys.argv[1]
