@@ -331,6 +331,8 @@ def main():
     # Algorithmic work per pivot: (m+1)(n+m+1) fp64 cells, each read + written
     # (16 B) and updated by one multiply + one subtract (2 flops) -- BASELINE.md §2.
     variant = _native.kernel_variant(m, n)
+    if shared and variant.startswith("lazy+") and not variant.startswith(("lazy+cluster", "lazy+hbm")):
+        variant = variant[len("lazy+"):]          # support mode keeps the dense kernel for these shapes
     bpp = bytes_per_pivot(m, n)
     fpp = 2 * (m + 1) * (n + m + 1)
     secs = step_ms / 1e3

@@ -112,8 +112,6 @@ bool plan_tableau(int m, int n, Plan *p) {
     else if (rpl <= 16) { p->fn = blp::tableau_kernel<16, false, 512>; p->name = "hbm_rpl16"; maxt = 512; }
     else if (rpl <= 32) { p->fn = blp::tableau_kernel<32, false, 256>; p->name = "hbm_rpl32"; maxt = 256; }
     else return false;
-    // HBM-streamed shapes: the exact lazy tableau first, this kernel for what it defers
-    p->lazy = !smem_tab && env_int("BLP_FORCE_HBM", 0) == 0 && blp_cluster::lazy_enabled(m, n);
     // threads: resident CTAs of one SM hold ~32 warps (register budget ~64/thread),
     // never more warps than columns
     const int ncols = n + m + 1;
@@ -126,11 +124,6 @@ bool plan_tableau(int m, int n, Plan *p) {
     const blp::TabLayout L = blp::make_tab_layout(m, n, p->threads / 32, smem_tab);
     p->smem = L.bytes;
     p->slot = smem_tab ? 0 : (long long)L.ncols * L.ld;
-    if (p->lazy) {
-        static thread_local std::string name;
-        name = std::string("lazy+") + p->name;
-        p->name = name.c_str();
-    }
     return true;
 }
 
@@ -223,10 +216,29 @@ bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
     if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
-    if ((any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p)) return true;
-    if ((any || strcmp(force, "warplp") == 0 || strcmp(force, "regtile") == 0) && plan_regtile(m, n, p)) return true;
-    if ((any || strcmp(force, "cluster") == 0) && plan_cluster(m, n, !any, p)) return true;
-    return plan_tableau(m, n, p);
+    bool dense = (any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p);
+    if (!dense) {
+        if ((any || strcmp(force, "warplp") == 0 || strcmp(force, "regtile") == 0) && plan_regtile(m, n, p)) return true;
+        if ((any || strcmp(force, "cluster") == 0) && plan_cluster(m, n, !any, p)) return true;   // lazy inside
+        dense = plan_tableau(m, n, p);
+    }
+    if (!dense) return false;
+    // The exact lazy tableau first (single-phase LPs within 64 pivots), the dense kernel for
+    // what it defers: always ahead of the HBM-streamed kernel; ahead of the 33..128-row and
+    // shared-memory kernels for independent LPs unless a family is forced.  Measured
+    // (scripts/lazy_vs_dense.py, device-resident): the reference's random workload 1.3x faster
+    // at 50 x 50, 2x at 64 x 64, 3.5x at 100 x 100 (5-8 pivots); C3 unchanged (phase-1 LPs
+    // are handed over after one look at b); but the support-function batch (C4, 64 x 32,
+    // ~24 pivots on a small tableau) 1.55x slower -- so support mode keeps the dense kernel.
+    p->lazy = blp_cluster::lazy_enabled(m, n) &&
+              (p->slot != 0 ? env_int("BLP_FORCE_HBM", 0) == 0
+                            : (any && m > 32 && env_int("BLP_LAZY_SMALL", 1) != 0));
+    if (p->lazy) {
+        static thread_local std::string name;
+        name = std::string("lazy+") + p->name;
+        p->name = name.c_str();
+    }
+    return true;
 }
 
 struct DeviceInfo {
@@ -308,6 +320,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     if (grid > count) grid = count;
     int *defer_list = nullptr, *defer_count = nullptr;
     void *lazy_ws = nullptr;
+    if (P.lazy && shared_Ab && P.slot == 0) P.lazy = false;   // support mode: dense (see plan_launch)
     if (P.lazy) {   // the lazy kernel over the batch; this kernel then solves only what it defers
         const cudaError_t le = blp_cluster::launch_lazy(Bproto(A, b, c, count, m, n, shared_Ab, lim, status, objective,
                                                                x, it1, it2), stream, &defer_list, &defer_count, &lazy_ws);

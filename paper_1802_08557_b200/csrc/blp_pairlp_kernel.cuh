@@ -446,8 +446,8 @@ pairlp_kernel(Batch B) {
     for (;;) {
         if (threadIdx.x == 0) s_lp = atomicAdd(B.next_lp, 1);
         __syncthreads();
-        const long long lp = s_lp;
-        if (lp >= B.count) break;
+        if (s_lp >= batch_count(B)) break;    // the deferred LPs when launched after the lazy kernel
+        const long long lp = batch_lp(B, s_lp);
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;

@@ -400,3 +400,18 @@ def test_lazy_ahead_of_hbm_kernel():
     got = batch_solve_arrays(A, b, c)
     compare(_native_dict(got), oracle.solve_batch(A, b, c), "lazy+hbm 600x600")
     assert (got.status[-3:] == 2).all()
+
+
+@pytest.mark.parametrize("m,n", [(50, 50), (64, 64), (100, 100), (64, 32), (90, 150)])
+def test_lazy_ahead_of_register_and_smem_kernels(m, n):
+    """Default path for 33..128-row shapes: the lazy tableau takes the single-phase LPs, the
+    pair/quad/smem kernel the ones it defers (phase 1, or > 64 pivots): equal to the oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, batch_solve_arrays
+    assert _native.kernel_variant(m, n).startswith("lazy+")
+    A, b, c = _single_phase_mix(m, n, seed=m * 13 + n)
+    from paper_1802_08557_b200 import workloads
+    A2, b2, c2 = workloads.afiro_arrays(60, seed=m + n, m=m, n=n)           # two-phase: deferred at once
+    A, b, c = np.concatenate([A, A2]), np.concatenate([b, b2]), np.concatenate([c, c2])
+    want = oracle.solve_batch(A, b, c)
+    compare(_native_dict(batch_solve_arrays(A, b, c)), want, f"lazy-first {m}x{n}")

@@ -38,8 +38,9 @@ def test_host_only_entry_points():
     assert lib.blp_launch_count() >= 0
 
 
-@pytest.mark.parametrize("m,n,family", [(5, 5, "warplp"), (28, 32, "warplp"), (64, 32, "pairlp"),
-                                        (100, 100, "quadlp"), (50, 50, "pairlp"), (100, 150, "smem"), (500, 500, "lazy+cluster"),
+@pytest.mark.parametrize("m,n,family", [(5, 5, "warplp"), (28, 32, "warplp"), (64, 32, "lazy+pairlp"),
+                                        (100, 100, "lazy+quadlp"), (50, 50, "lazy+pairlp"), (100, 150, "lazy+smem"),
+                                        (500, 500, "lazy+cluster"),
                                         (150, 150, "lazy+cluster"), (600, 600, "lazy+hbm")])
 def test_kernel_variant_selection(m, n, family):
     assert _native.kernel_variant(m, n).startswith(family)
