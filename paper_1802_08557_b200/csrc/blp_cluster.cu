@@ -147,9 +147,10 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
 
 cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_list, int **defer_count, void **ws_out) {
     using LazyFn = void (*)(blp::Batch);
-    // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget;
-    // C5 1e4: 256 -> 6.73 ms, 512 -> 6.96, 128 -> 7.71)
-    const int nt = env_int("BLP_LAZY_NT", 256);
+    // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget).
+    // C5 1e4: 256 -> 6.73 ms, 512 -> 6.96, 128 -> 7.71; random 100 x 100, 2e4: 128 -> 0.95,
+    // 256 -> 1.21, 512 -> 1.89; 64 x 64: 128 -> 0.51, 256 -> 0.77
+    const int nt = env_int("BLP_LAZY_NT", B.m <= 128 ? 128 : 256);
     LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2> : (nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
                                                                           : (LazyFn)blp::lazy_kernel<256, 4>);
     const int threads = nt == 512 ? 512 : (nt == 128 ? 128 : 256);
