@@ -225,11 +225,11 @@ bool plan_launch(int m, int n, Plan *p) {
     if (!dense) return false;
     // The exact lazy tableau first (single-phase LPs within 64 pivots), the dense kernel for
     // what it defers: always ahead of the HBM-streamed kernel; ahead of the 33..128-row and
-    // shared-memory kernels for independent LPs unless a family is forced.  Measured
-    // (scripts/lazy_vs_dense.py, device-resident): the reference's random workload 1.3x faster
-    // at 50 x 50, 2x at 64 x 64, 3.5x at 100 x 100 (5-8 pivots); C3 unchanged (phase-1 LPs
-    // are handed over after one look at b); but the support-function batch (C4, 64 x 32,
-    // ~24 pivots on a small tableau) 1.55x slower -- so support mode keeps the dense kernel.
+    // shared-memory kernels unless a family is forced.  Measured
+    // (scripts/lazy_vs_dense.py, device-resident): the reference's random workload 2.5x faster
+    // at 50 x 50, 3.6x at 64 x 64, 4.5x at 100 x 100 (5-8 pivots); the support-function batch
+    // (C4, 64 x 32, ~24 pivots) 1.18x; C3 unchanged (phase-1 LPs are handed over after one
+    // look at b).
     p->lazy = blp_cluster::lazy_enabled(m, n) &&
               (p->slot != 0 ? env_int("BLP_FORCE_HBM", 0) == 0
                             : (any && m > 32 && env_int("BLP_LAZY_SMALL", 1) != 0));
@@ -320,7 +320,6 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     if (grid > count) grid = count;
     int *defer_list = nullptr, *defer_count = nullptr;
     void *lazy_ws = nullptr;
-    if (P.lazy && shared_Ab && P.slot == 0) P.lazy = false;   // support mode: dense (see plan_launch)
     if (P.lazy) {   // the lazy kernel over the batch; this kernel then solves only what it defers
         const cudaError_t le = blp_cluster::launch_lazy(Bproto(A, b, c, count, m, n, shared_Ab, lim, status, objective,
                                                                x, it1, it2), stream, &defer_list, &defer_count, &lazy_ws);

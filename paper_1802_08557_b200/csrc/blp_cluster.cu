@@ -149,11 +149,16 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     using LazyFn = void (*)(blp::Batch);
     // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget).
     // C5 1e4: 256 -> 6.73 ms, 512 -> 6.96, 128 -> 7.71; random 100 x 100, 2e4: 128 -> 0.95,
-    // 256 -> 1.21, 512 -> 1.89; 64 x 64: 128 -> 0.51, 256 -> 0.77
-    const int nt = env_int("BLP_LAZY_NT", B.m <= 128 ? 128 : 256);
-    LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2> : (nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
-                                                                          : (LazyFn)blp::lazy_kernel<256, 4>);
-    const int threads = nt == 512 ? 512 : (nt == 128 ? 128 : 256);
+    // 256 -> 1.21, 64 -> 0.99; 64 x 64: 64 -> 0.42, 128 -> 0.51, 32 -> 0.48; support mode (no
+    // per-LP scan of A) C4 1e6: 32 -> 65.4 ms, 64 -> 70.7, 128 -> 81.5 (dense pairlp: 77.3)
+    const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 256));
+    const int nt = env_int("BLP_LAZY_NT", dflt);
+    LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2>
+              : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
+              : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16>
+              : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32>
+                          : (LazyFn)blp::lazy_kernel<256, 4>;
+    const int threads = (nt == 512 || nt == 128 || nt == 64 || nt == 32) ? nt : 256;
     const size_t smem = blp::make_lazy_layout(B.m, B.n).bytes;
     *ws_out = nullptr;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
