@@ -415,3 +415,16 @@ def test_lazy_ahead_of_register_and_smem_kernels(m, n):
     A, b, c = np.concatenate([A, A2]), np.concatenate([b, b2]), np.concatenate([c, c2])
     want = oracle.solve_batch(A, b, c)
     compare(_native_dict(batch_solve_arrays(A, b, c)), want, f"lazy-first {m}x{n}")
+
+
+def test_lazy_path_honours_solver_limits():
+    """Limits flow through the lazy kernel exactly as through the dense ones: no
+    anti-cycling, a custom degenerate-pivot trigger, small iteration caps."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import SolverLimits, batch_solve_arrays
+    A, b, c = _single_phase_mix(100, 100, seed=77)
+    for kw in (dict(anti_cycling=False, max_iterations=30), dict(degenerate_pivot_limit=2),
+               dict(degenerate_pivot_limit=1, max_iterations=50)):
+        want = oracle.solve_batch(A, b, c, **kw)
+        got = batch_solve_arrays(A, b, c, SolverLimits(**kw))
+        compare(_native_dict(got), want, f"lazy limits {kw}")
