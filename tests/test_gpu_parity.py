@@ -428,3 +428,32 @@ def test_lazy_path_honours_solver_limits():
         want = oracle.solve_batch(A, b, c, **kw)
         got = batch_solve_arrays(A, b, c, SolverLimits(**kw))
         compare(_native_dict(got), want, f"lazy limits {kw}")
+
+
+@pytest.mark.parametrize("cfg", ["afiro", "support", "lazy500"])
+def test_pageable_host_buffers_match_pinned(cfg, monkeypatch):
+    """Pageable numpy buffers go through the pinned staging ring (parallel memcpy,
+    several sub-batches in flight); results are bit-identical to the pinned path."""
+    import ctypes
+    from paper_1802_08557_b200 import _native, workloads
+    if cfg == "afiro":
+        A, b, c = workloads.afiro_arrays(30_000, seed=4)
+        shared = False
+    elif cfg == "support":
+        A, b = workloads.support_polytope()
+        c = workloads.support_directions(50_000)
+        shared = True
+    else:
+        A, b, c = workloads.random_arrays(500, 40, seed=41)
+        shared = False
+    monkeypatch.setenv("BLP_STAGE_MB", "8")          # many sub-batches through a 4-slot ring
+    lim = _native.make_limits()
+    got = _native.solve_host(np.ascontiguousarray(A), np.ascontiguousarray(b), np.ascontiguousarray(c), lim,
+                             shared_Ab=shared, out={k: np.zeros_like(v) for k, v in
+                                                    _native.alloc_outputs(len(c), c.shape[1]).items()})
+    pin = {k: _native.alloc_host(v.shape, v.dtype) for k, v in (("A", A), ("b", b), ("c", c))}
+    for k, v in (("A", A), ("b", b), ("c", c)):
+        pin[k][...] = v
+    ref = _native.solve_host(pin["A"], pin["b"], pin["c"], lim, shared_Ab=shared)
+    for k in ("status", "objective", "x", "it1", "it2"):
+        assert np.array_equal(got[k], ref[k], equal_nan=True), k
