@@ -263,32 +263,30 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
     shapes = {(lp.m, lp.n) for lp in lps}
     if len(shapes) > 1:
         raise HeterogeneousBatch(f"batch mixes LP shapes {sorted(shapes)}")
-    if lps:
-        m, n = next(iter(shapes))
-        worst_artificial = max(int(np.sum(np.asarray(lp.b) < 0)) for lp in lps)
-        lp_bytes = lp_memory_bytes(m, n, num_slack=m, num_artificial=worst_artificial,
-                                   data_size_bytes=config.data_size_bytes)
-    else:
-        lp_bytes = 1
-    plan = plan_chunks(len(lps), lp_bytes, config)
     if not lps:
-        return BatchReport(outcomes=[], plan=plan, chunk_seconds=[], total_seconds=0.0)
-
-    started = time.perf_counter()        # like batch.py:157, the timer covers everything after planning
-    # Pack once.  The reference raises at the first invalid LP in index order
-    # (validate() inside solve()); a mis-shaped A stops packing there, and
-    # non-finite entries are flagged by the kernel (BLP_STATUS_INVALID).
+        return BatchReport(outcomes=[], plan=plan_chunks(0, 1, config), chunk_seconds=[], total_seconds=0.0)
+    m, n = next(iter(shapes))
+    # Pack once, straight into page-locked buffers (the library's H2D copies then run at
+    # full PCIe rate).  The reference raises at the first invalid LP in index order
+    # (validate() inside solve()); a mis-shaped A stops packing there, and non-finite
+    # entries are flagged by the kernel (BLP_STATUS_INVALID).
     bad_shape = _first_bad_shape(lps, m, n)
     limit = bad_shape if bad_shape >= 0 else len(lps)
-    # packed straight into page-locked buffers: the library's H2D copies run at full PCIe rate
     A = _native.alloc_host((limit, m, n))
     b = _native.alloc_host((limit, m))
     c = _native.alloc_host((limit, n))
-    for k in range(limit):
-        lp = lps[k]
-        A[k] = lp.A
-        b[k] = lp.b
-        c[k] = lp.c
+    if limit:
+        np.stack([lp.A for lp in lps[:limit]], out=A)
+        np.stack([lp.b for lp in lps[:limit]], out=b)
+        np.stack([lp.c for lp in lps[:limit]], out=c)
+    # the chunk plan with the batch-worst artificial count (batch.py:146-153), from the packed b
+    worst_artificial = int((b < 0).sum(axis=1).max()) if limit else 0
+    if bad_shape >= 0:
+        worst_artificial = max(worst_artificial, max(int(np.sum(np.asarray(lp.b) < 0)) for lp in lps[limit:]))
+    lp_bytes = lp_memory_bytes(m, n, num_slack=m, num_artificial=worst_artificial,
+                               data_size_bytes=config.data_size_bytes)
+    plan = plan_chunks(len(lps), lp_bytes, config)
+    started = time.perf_counter()        # like batch.py:157, the timer covers everything after planning
     if bad_shape >= 0:
         if bad_shape:
             res = _solve_sharded(A, b, c, config.limits, config.devices, shared_Ab=False)
