@@ -31,7 +31,7 @@ import numpy as np
 from . import _native
 from .model import SolveOutcome, StandardFormLP, STATUS_BY_CODE, invalid_message, validate
 from .shard import shard_bounds
-from .simplex import PHASE1_UNBOUNDED_MESSAGE, SolverLimits, outcome_from_arrays
+from .simplex import PHASE1_UNBOUNDED_MESSAGE, SolverLimits, outcome_from_arrays, outcomes_from_arrays
 
 # Column ceiling of the paper's one-block-per-LP Kepler kernel (batch.py:25-29);
 # informational, as in the reference.  The B200 kernels have no such limit.
@@ -146,7 +146,7 @@ class BatchArrays:
 
     def outcomes(self) -> list[SolveOutcome]:
         d = self._as_dict()
-        return [outcome_from_arrays(d, k) for k in range(len(self.status))]
+        return outcomes_from_arrays(d, 0, len(self.status))
 
     def status_counts(self) -> dict[str, int]:
         codes, counts = np.unique(self.status, return_counts=True)
@@ -300,7 +300,7 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
         res = _solve_sharded(A[start:end], b[start:end], c[start:end], config.limits,
                              config.devices, shared_Ab=False)
         _raise_for_errors(res, lambda k: lps[start + k])
-        outcomes[start:end] = [outcome_from_arrays(res, k) for k in range(end - start)]
+        outcomes[start:end] = outcomes_from_arrays(res, 0, end - start)
         chunk_seconds.append(time.perf_counter() - t0)
     total = time.perf_counter() - started
     return BatchReport(outcomes=outcomes, plan=plan, chunk_seconds=chunk_seconds, total_seconds=total)

@@ -60,6 +60,28 @@ def outcome_from_arrays(res: dict, k: int) -> SolveOutcome:
     return SolveOutcome(status, iterations_phase1=int(res["it1"][k]), iterations_phase2=int(res["it2"][k]))
 
 
+def outcomes_from_arrays(res: dict, start: int, end: int) -> list[SolveOutcome]:
+    """outcome_from_arrays for LPs [start, end) of a native result, in bulk: scalars via
+    tolist(), each primal point a row view of one copy of x (the reference's point is a
+    view too: ``x[:n]`` of its per-LP vector, simplex.py:146-151)."""
+    codes = res["status"][start:end].tolist()
+    if 4 in codes:
+        raise RuntimeError(PHASE1_UNBOUNDED_MESSAGE)
+    obj = res["objective"][start:end].tolist()
+    it1 = res["it1"][start:end].tolist()
+    it2 = res["it2"][start:end].tolist()
+    xs = np.array(res["x"][start:end], dtype=np.float64)
+    opt = Status.OPTIMAL
+    out = []
+    for k, code in enumerate(codes):
+        st = STATUS_BY_CODE[code]
+        if st is opt:
+            out.append(SolveOutcome(st, obj[k], xs[k], it1[k], it2[k]))
+        else:
+            out.append(SolveOutcome(st, None, None, it1[k], it2[k]))
+    return out
+
+
 def solve(lp: StandardFormLP, limits: SolverLimits = SolverLimits(), device: int = 0) -> SolveOutcome:
     """Two-phase simplex solve of one standard-form LP on the GPU."""
     violations = validate(lp)
