@@ -457,3 +457,22 @@ def test_pageable_host_buffers_match_pinned(cfg, monkeypatch):
     ref = _native.solve_host(pin["A"], pin["b"], pin["c"], lim, shared_Ab=shared)
     for k in ("status", "objective", "x", "it1", "it2"):
         assert np.array_equal(got[k], ref[k], equal_nan=True), k
+
+
+def test_random_shapes_default_dispatch():
+    """Thirty random (m, n) shapes through the default dispatcher (every family, the
+    lazy-first path included), single- and two-phase LPs mixed: equal to the oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import batch_solve_arrays, workloads
+    rng = np.random.default_rng(2026)
+    for _ in range(30):
+        m, n = int(rng.integers(1, 161)), int(rng.integers(1, 161))
+        A1, b1, c1 = workloads.afiro_arrays(12, seed=int(rng.integers(1 << 30)), m=max(m, 2), n=n)
+        A1, b1 = A1[:, :m], b1[:, :m]
+        A2, b2, c2 = workloads.random_arrays(max(m, n), 12, seed=int(rng.integers(1 << 30)))
+        A2, b2, c2 = A2[:, :m, :n], b2[:, :m], c2[:, :n]
+        A = np.ascontiguousarray(np.concatenate([A1, A2]))
+        b = np.ascontiguousarray(np.concatenate([b1, b2]))
+        c = np.ascontiguousarray(np.concatenate([c1, c2]))
+        want = oracle.solve_batch(A, b, c)
+        compare(_native_dict(batch_solve_arrays(A, b, c)), want, f"random shape {m}x{n}")
