@@ -476,3 +476,43 @@ def test_random_shapes_default_dispatch():
         c = np.ascontiguousarray(np.concatenate([c1, c2]))
         want = oracle.solve_batch(A, b, c)
         compare(_native_dict(batch_solve_arrays(A, b, c)), want, f"random shape {m}x{n}")
+
+
+def test_results_invariant_to_chunking_and_sharding(monkeypatch):
+    """The reference's determinism law (test_acceptance.py:178-195) for every path:
+    sub-batch counts, staging slot sizes, the object API's chunk plan and a two-shard
+    run (devices=(0, 0)) all give bit-identical outcomes -- dense, lazy and deferred LPs."""
+    from paper_1802_08557_b200 import BatchConfig, batch_solve, batch_solve_arrays, standard_form, workloads
+    A1, b1, c1 = workloads.afiro_arrays(3000, seed=91, m=60, n=40)        # two-phase: deferred to pairlp
+    A2, b2, c2 = workloads.random_arrays(60, 3000, seed=92)                 # single phase: lazy
+    A = np.concatenate([A1, A2[:, :, :40]])
+    b = np.concatenate([b1, b2])
+    c = np.concatenate([c1, c2[:, :40]])
+    ref = _native_dict(batch_solve_arrays(A, b, c))
+    variants = [dict(BLP_HOST_CHUNKS="3"), dict(BLP_HOST_CHUNKS="64"), dict(BLP_STAGE_MB="1"), dict(BLP_STAGE="0")]
+    for env in variants:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        got = _native_dict(batch_solve_arrays(A, b, c))
+        for k in ref:
+            assert np.array_equal(ref[k], got[k], equal_nan=True), (env, k)
+        for k in env:
+            monkeypatch.delenv(k)
+    got = _native_dict(batch_solve_arrays(A, b, c, devices=(0, 0)))
+    for k in ref:
+        assert np.array_equal(ref[k], got[k], equal_nan=True), ("sharded", k)
+    lps = [standard_form(c[i], A[i], b[i]) for i in range(0, len(c), 7)]
+    r1 = batch_solve(lps)
+    r2 = batch_solve(lps, BatchConfig(memory_budget_bytes=lp_bytes_for(60, 40) * 37))
+    assert r2.plan.count > 1
+    for o1, o2 in zip(r1.outcomes, r2.outcomes):
+        assert o1.status == o2.status and o1.iterations_phase1 == o2.iterations_phase1
+        assert o1.iterations_phase2 == o2.iterations_phase2
+        assert (o1.primal_point is None) == (o2.primal_point is None)
+        if o1.primal_point is not None:
+            assert np.array_equal(o1.primal_point, o2.primal_point) and o1.objective_value == o2.objective_value
+
+
+def lp_bytes_for(m, n):
+    from paper_1802_08557_b200 import lp_memory_bytes
+    return lp_memory_bytes(m, n, num_slack=m, num_artificial=m)
