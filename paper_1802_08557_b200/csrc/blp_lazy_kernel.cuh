@@ -133,11 +133,13 @@ lazy_kernel(Batch B) {
             const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
             const size_t n2 = (total - head) / 2;
             size_t q = tid;
-            for (; q + 3 * NT < n2; q += 4 * NT) {
-                const double2 v0 = __ldcs(A2 + q), v1 = __ldcs(A2 + q + NT), v2 = __ldcs(A2 + q + 2 * NT),
-                              v3 = __ldcs(A2 + q + 3 * NT);
-                nonfinite |= !(isfinite(v0.x) && isfinite(v0.y) && isfinite(v1.x) && isfinite(v1.y) &&
-                               isfinite(v2.x) && isfinite(v2.y) && isfinite(v3.x) && isfinite(v3.y));
+            constexpr int U = 4;                   // 16-byte loads in flight per thread
+            for (; q + (U - 1) * NT < n2; q += U * NT) {
+                double2 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = __ldcs(A2 + q + u * NT);
+#pragma unroll
+                for (int u = 0; u < U; ++u) nonfinite |= !(isfinite(v[u].x) && isfinite(v[u].y));
             }
             for (; q < n2; q += NT) {
                 const double2 v = __ldcs(A2 + q);
