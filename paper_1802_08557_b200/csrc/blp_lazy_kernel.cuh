@@ -37,6 +37,25 @@ namespace blp {
 
 constexpr int kLazyMaxPivots = 64;
 
+#ifndef LAZY_SCAN_U
+#define LAZY_SCAN_U 4
+#endif
+#ifndef LAZY_SCAN_MODE
+#define LAZY_SCAN_MODE 0
+#endif
+// One 16-byte load of the validation stream (read once: evict-first).
+__device__ __forceinline__ double2 lazy_scan_load(const double2 *p) {
+#if LAZY_SCAN_MODE == 1
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+#elif LAZY_SCAN_MODE == 2
+    return __ldcg(p);
+#else
+    return __ldcs(p);
+#endif
+}
+
 struct LazyPart {
     unsigned long long ckey[32];
     int cidx[32], cbl[32];
@@ -133,11 +152,11 @@ lazy_kernel(Batch B) {
             const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
             const size_t n2 = (total - head) / 2;
             size_t q = tid;
-            constexpr int U = 4;                   // 16-byte loads in flight per thread
+            constexpr int U = LAZY_SCAN_U;         // 16-byte loads in flight per thread
             for (; q + (U - 1) * NT < n2; q += U * NT) {
                 double2 v[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) v[u] = __ldcs(A2 + q + u * NT);
+                for (int u = 0; u < U; ++u) v[u] = lazy_scan_load(A2 + q + u * NT);
 #pragma unroll
                 for (int u = 0; u < U; ++u) nonfinite |= !(isfinite(v[u].x) && isfinite(v[u].y));
             }
