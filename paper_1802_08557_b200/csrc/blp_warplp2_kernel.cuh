@@ -13,6 +13,10 @@
 // into their lane, and price-out streams one row at a time through smem.
 #pragma once
 
+#ifndef WL2_PIPE
+#define WL2_PIPE 1   // C2 1e5: 8.43 -> 8.30 ms, and no spills
+#endif
+
 #include "blp_common.cuh"
 #include "blp_keys.cuh"
 #include "blp_warplp_kernel.cuh"
@@ -130,6 +134,38 @@ __device__ __forceinline__ void wl2_pivot(const WlpDims &D, Wl2State<R, S> &St, 
         St.a[c + 1] = __dsub_rn(St.a[c + 1], __dmul_rn(av, r2.y));
     }
     const double fs = mine ? 0.0 : av;     // row l of the smem columns already holds r
+#if WL2_PIPE
+    {
+        // software-pipelined: batch b+1 (4 columns + their pivot-row entries) is loaded
+        // before batch b is stored (tile and rvec share shared memory, so the compiler
+        // would otherwise order each load after every earlier store)
+        constexpr int K = 4, NB = (S + K - 1) / K;
+        const unsigned ca = (unsigned)__cvta_generic_to_shared(tile + D.lane);
+        const unsigned ra = (unsigned)__cvta_generic_to_shared(rvec + R);
+        double t[2][K], r[2][K];
+        auto load = [&](int b, int sl) {
+#pragma unroll
+            for (int k = 0; k < K; k += 2) {
+                const int c = b * K + k;
+                if (c < S) {
+                    lds_v2_f64(ra + 8u * c, r[sl][k], r[sl][k + 1]);
+                    t[sl][k] = lds_f64(ca + 8u * C::TS * c);
+                    if (c + 1 < S) t[sl][k + 1] = lds_f64(ca + 8u * C::TS * (c + 1));
+                }
+            }
+        };
+        load(0, 0);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            if (b + 1 < NB) load(b + 1, (b + 1) & 1);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int c = b * K + k;
+                if (c < S) sts_f64(ca + 8u * C::TS * c, __dsub_rn(t[b & 1][k], __dmul_rn(fs, r[b & 1][k])));
+            }
+        }
+    }
+#else
     double *col = tile + D.lane;
 #pragma unroll
     for (int c = 0; c < S; c += 2) {
@@ -138,6 +174,7 @@ __device__ __forceinline__ void wl2_pivot(const WlpDims &D, Wl2State<R, S> &St, 
         col[c * C::TS] = __dsub_rn(t0, __dmul_rn(fs, r2.x));
         col[(c + 1) * C::TS] = __dsub_rn(t1, __dmul_rn(fs, r2.y));
     }
+#endif
 #pragma unroll
     for (int c = 0; c < R; c += 2) ld_shared_v2_if(mine, rv + 8u * c, St.a[c], St.a[c + 1]);
     __syncwarp();
