@@ -93,8 +93,28 @@ __host__ __device__ inline long long lazy_scratch_doubles(int m, int n) {
 
 // Initial tableau cell a^0_ij of a single-phase LP (all row signs +1):
 // [A | I] (tableau.py:149-170).
+// Load-path knobs, measured (C5 / C4 / random 100x100): plain loads 5.74 / 65.0 / 0.83 ms;
+// __ldcg history 6.39 / 73.2 / 0.95; __ldg for A no change.
+#ifndef LAZY_HIST_MODE
+#define LAZY_HIST_MODE 0
+#endif
+#ifndef LAZY_A_MODE
+#define LAZY_A_MODE 0
+#endif
 __device__ __forceinline__ double lazy_a0(const double *Ag, int n, int i, int j) {
+#if LAZY_A_MODE == 1
+    return j < n ? __ldg(Ag + (size_t)i * n + j) : ((j - n == i) ? 1.0 : 0.0);
+#else
     return j < n ? Ag[(size_t)i * n + j] : ((j - n == i) ? 1.0 : 0.0);
+#endif
+}
+// A replay-history load (written earlier by this CTA)
+__device__ __forceinline__ double lazy_h(const double *p) {
+#if LAZY_HIST_MODE == 1
+    return __ldcg(p);
+#else
+    return *p;
+#endif
 }
 
 template <int NT, int MINB>
@@ -228,8 +248,9 @@ lazy_kernel(Batch B) {
                 const double *Rcol = Rh + e;
                 for (int i = tid; i < m; i += NT) {
                     const int t0 = lastpiv[i];
-                    double a = t0 ? Rcol[(size_t)(t0 - 1) * nv] : lazy_a0(Ag, n, i, e);
-                    for (int t = t0; t < k; ++t) a = __dsub_rn(a, __dmul_rn(Fh[(size_t)t * m + i], Rcol[(size_t)t * nv]));
+                    double a = t0 ? lazy_h(Rcol + (size_t)(t0 - 1) * nv) : lazy_a0(Ag, n, i, e);
+                    for (int t = t0; t < k; ++t)
+                        a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + i), lazy_h(Rcol + (size_t)t * nv)));
                     fcur[i] = a;
                     Fh[(size_t)k * m + i] = a;
                     const unsigned long long key = key_min(ratio_entry(rhs[i], a));
@@ -266,8 +287,9 @@ lazy_kernel(Batch B) {
                 int ci = kNone, cb = kNone;
                 double *Rk = Rh + (size_t)k * nv;
                 for (int j = tid; j < nv; j += NT) {
-                    double a = t0l ? Rh[(size_t)(t0l - 1) * nv + j] : lazy_a0(Ag, n, l, j);
-                    for (int t = t0l; t < k; ++t) a = __dsub_rn(a, __dmul_rn(Fh[(size_t)t * m + l], Rh[(size_t)t * nv + j]));
+                    double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * nv + j) : lazy_a0(Ag, n, l, j);
+                    for (int t = t0l; t < k; ++t)
+                        a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + l), lazy_h(Rh + (size_t)t * nv + j)));
                     const double r = div_entry(a, pe);
                     Rk[j] = r;
                     const double v = __dsub_rn(rc[j], __dmul_rn(rce, r));
