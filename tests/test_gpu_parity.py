@@ -516,3 +516,36 @@ def test_results_invariant_to_chunking_and_sharding(monkeypatch):
 def lp_bytes_for(m, n):
     from paper_1802_08557_b200 import lp_memory_bytes
     return lp_memory_bytes(m, n, num_slack=m, num_artificial=m)
+
+
+@pytest.mark.parametrize("shape,shared", [((150, 150), False), ((64, 32), True), ((100, 100), False)])
+def test_device_api_equals_host_api_lazy_paths(shape, shared):
+    """The device entry point (torch tensors, caller's stream) takes the same lazy-first
+    dispatch as the host one: identical results, independent and support mode."""
+    from paper_1802_08557_b200 import SolverLimits, _native, workloads
+    m, n = shape
+    if shared:
+        A, b = workloads.support_polytope()
+        c = workloads.support_directions(5000)
+    else:
+        A1, b1, c1 = workloads.random_arrays(max(m, n), 200, seed=m + n)
+        A2, b2, c2 = workloads.afiro_arrays(50, seed=m * n, m=m, n=n)
+        A = np.concatenate([A1[:, :m, :n], A2])
+        b = np.concatenate([b1[:, :m], b2])
+        c = np.concatenate([c1[:, :n], c2])
+    A, b, c = (np.ascontiguousarray(v) for v in (A, b, c))
+    host = _native.solve_host(A, b, c, SolverLimits().to_native(), shared_Ab=shared)
+    dev = torch.device("cuda:0")
+    tA, tb, tc = (torch.from_numpy(v).to(dev) for v in (A, b, c))
+    cnt = len(c)
+    out = dict(status=torch.empty(cnt, dtype=torch.int8, device=dev),
+               objective=torch.empty(cnt, dtype=torch.float64, device=dev),
+               x=torch.empty(cnt, n, dtype=torch.float64, device=dev),
+               it1=torch.empty(cnt, dtype=torch.int32, device=dev),
+               it2=torch.empty(cnt, dtype=torch.int32, device=dev))
+    stream = torch.cuda.Stream()
+    _native.solve_device(tA, tb, tc, SolverLimits().to_native(), out, shared_Ab=shared, stream=stream)
+    stream.synchronize()
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    for k in ("status", "objective", "x", "it1", "it2"):
+        assert np.array_equal(got[k], host[k], equal_nan=True), (shape, k)
