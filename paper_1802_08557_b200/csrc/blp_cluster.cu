@@ -151,7 +151,8 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     // C5 1e4: 256 -> 6.73 ms, 512 -> 6.96, 128 -> 7.71; random 100 x 100, 2e4: 128 -> 0.95,
     // 256 -> 1.21, 64 -> 0.99; 64 x 64: 64 -> 0.42, 128 -> 0.51, 32 -> 0.48; support mode (no
     // per-LP scan of A) C4 1e6: 32 -> 65.4 ms, 64 -> 70.7, 128 -> 81.5 (dense pairlp: 77.3)
-    const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 256));
+    // (after the unrolled validation scan, C5: 512 -> 5.43 ms, 256 -> 5.75)
+    const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 512));
     const int nt = env_int("BLP_LAZY_NT", dflt);
     LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2>
               : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
