@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs, procs = [], []
     for src in SOURCES:
         obj = OBJDIR / (src.stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
+        extra = os.environ.get("BLP_EXTRA_NVCC", "").split()      # experiment knobs (-D...), A/B builds only
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, *(["-Xptxas", "-v"] if verbose else []), "-c", "-o", str(obj), str(src)]
         procs.append((cmd, subprocess.Popen(cmd)))
         objs.append(obj)
     for cmd, p in procs:

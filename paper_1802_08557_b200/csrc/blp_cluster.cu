@@ -48,7 +48,7 @@ bool shape_fits(int m, int n) {
 }
 
 bool lazy_enabled(int m, int n) {
-    return env_int("BLP_LAZY", 1) != 0 && blp::make_lazy_layout(m, n).bytes <= kMaxDynSmem;
+    return env_int("BLP_LAZY", 1) != 0 && blp::lazy_smem_bytes(m, n, 0, 512, 1) <= kMaxDynSmem;
 }
 
 const char *variant_name(int m, int n) {
@@ -154,16 +154,35 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     // (after the unrolled validation scan, C5: 512 -> 5.43 ms, 256 -> 5.75)
     const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 512));
     const int nt = env_int("BLP_LAZY_NT", dflt);
-    LazyFn fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2>
-              : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8>
-              : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16>
-              : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32>
-                          : (LazyFn)blp::lazy_kernel<256, 4>;
+    // BLP_LAZY_WS=1: the warp-specialised bulk-copy validation stream (measured slower on
+    // C5: 6.7 vs 6.0 ms -- the solve, not the stream, bounds an LP); the staged replay
+    // (RP=1) only for the shared polytope (C4 1e6: 60.2 vs 65.0 ms; C5 5.87 vs 5.43,
+    // random 100 x 100 0.98 vs 0.83)
+    const int ws_mode = (nt == 512 && !B.shared_Ab && env_int("BLP_LAZY_WS", 0)) ? 1 : 0;
+    const int rp = env_int("BLP_LAZY_RP", B.shared_Ab ? 1 : 0) ? 1 : 0;
+    LazyFn fn;
+    if (ws_mode) fn = rp ? (LazyFn)blp::lazy_kernel<512, 2, 1, 1> : (LazyFn)blp::lazy_kernel<512, 2, 1, 0>;
+    else if (rp)
+        fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2, 0, 1>
+           : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8, 0, 1>
+           : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16, 0, 1>
+           : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32, 0, 1>
+                       : (LazyFn)blp::lazy_kernel<256, 4, 0, 1>;
+    else
+        fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2, 0, 0>
+           : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8, 0, 0>
+           : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16, 0, 0>
+           : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32, 0, 0>
+                       : (LazyFn)blp::lazy_kernel<256, 4, 0, 0>;
     const int threads = (nt == 512 || nt == 128 || nt == 64 || nt == 32) ? nt : 256;
-    const size_t smem = blp::make_lazy_layout(B.m, B.n).bytes;
+    const size_t smem = blp::lazy_smem_bytes(B.m, B.n, ws_mode, threads, rp);
     *ws_out = nullptr;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // BLP_LAZY_CARVEOUT: shared-memory share of the L1/shared array in percent (-1: driver's choice)
+    const int carve = env_int("BLP_LAZY_CARVEOUT", -1);
+    if (carve >= 0 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve)) != cudaSuccess)
+        return e;
     int dev = 0, sms = 0, occ = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
@@ -194,8 +213,8 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
         e = cudaGetLastError();
     }
     if (env_int("BLP_VERBOSE", 0))
-        fprintf(stderr, "blp lazy: m=%d n=%d grid=%lld x %d (%d per SM) smem=%zu scratch=%.1f MB\n", B.m, B.n, grid,
-                threads, occ, smem, grid * stride * 8.0 / 1e6);
+        fprintf(stderr, "blp lazy: m=%d n=%d grid=%lld x %d (%d per SM, ws=%d rp=%d) smem=%zu scratch=%.1f MB\n", B.m, B.n,
+                grid, threads, occ, ws_mode, rp, smem, grid * stride * 8.0 / 1e6);
     if (e == cudaSuccess && B.shared_Ab && (long long)B.m * B.n > 0) {
         // support mode: the shared polytope is validated once by finish_lazy, after the
         // dense launch (its flags start cleared here)

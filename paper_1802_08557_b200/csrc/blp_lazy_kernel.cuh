@@ -117,7 +117,57 @@ __device__ __forceinline__ double lazy_h(const double *p) {
 #endif
 }
 
-template <int NT, int MINB>
+// Replay a cell's update history from pivot t to k-1: a -= v_t * h[t], v_t
+// loaded from p + t*stride (this cell's own history, coalesced across the
+// warp), h the staged broadcast operand.  Loads are issued 8 at a time so a
+// history of k pivots costs k/8 L2 round trips, not k.
+__device__ __forceinline__ double lazy_replay(double a, const double *p, size_t stride, const double *h, int t, int k) {
+    for (; t < k; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = t + u < k ? lazy_h(p + (size_t)(t + u) * stride) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t + u < k) a = __dsub_rn(a, __dmul_rn(v[u], h[t + u]));
+    }
+    return a;
+}
+// Warp-specialised validation stream (WS = 1): the last kLazyScanWarps warps of
+// the CTA stream the LP's A through a shared-memory ring filled by bulk async
+// copies (cp.async.bulk, completion on an mbarrier per stage) and check it,
+// while the other warps run the pivots of the same LP (named barrier 1), so an
+// LP costs max(stream, solve) instead of their sum; the in-flight bytes are the
+// ring's (kLazyRing x kLazyChunk per CTA), not registers.
+constexpr int kLazyScanWarps = 4;
+constexpr int kLazyRing = 4;
+constexpr int kLazyChunk = 16384;
+// Per-warp staging of the replay's broadcast operand (kLazyMaxPivots doubles per
+// warp) follows the layout; the ring follows that.
+__host__ __device__ inline size_t lazy_stage_bytes(int nt, int rp) { return rp ? (size_t)(nt / 32) * kLazyMaxPivots * 8 : 0; }
+__host__ __device__ inline size_t lazy_ring_offset(const LazyLayout &L, int nt, int rp) {
+    return (L.bytes + lazy_stage_bytes(nt, rp) + 127) / 128 * 128;
+}
+__host__ __device__ inline size_t lazy_smem_bytes(int m, int n, int ws, int nt, int rp) {
+    const LazyLayout L = make_lazy_layout(m, n);
+    return ws ? lazy_ring_offset(L, nt, rp) + (size_t)kLazyRing * kLazyChunk : L.bytes + lazy_stage_bytes(nt, rp);
+}
+__device__ __forceinline__ void lazy_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void lazy_mbar_wait(unsigned bar, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void lazy_bulk_load(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+template <int NT, int MINB, int WS, int RP>
 __global__ void __launch_bounds__(NT, MINB)
 lazy_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -132,7 +182,23 @@ lazy_kernel(Batch B) {
     LazyPart *P = reinterpret_cast<LazyPart *>(smem + L.off_part);
     long long *s_lp = reinterpret_cast<long long *>(smem + L.off_misc);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = NT / 32;
+    constexpr int PT = WS ? NT - 32 * kLazyScanWarps : NT;    // pivot threads
+    constexpr int NW = PT / 32;
+    static_assert(!WS || PT >= 64, "WS needs pivot warps");
+    int *s_res = reinterpret_cast<int *>(smem + L.off_misc + 8);             // status, iterations, deferred
+    unsigned long long *fullb = reinterpret_cast<unsigned long long *>(smem + L.off_misc + 32);
+    const unsigned ring = (unsigned)__cvta_generic_to_shared(smem + lazy_ring_offset(L, NT, RP));
+    double *hw = reinterpret_cast<double *>(smem + L.bytes) + warp * kLazyMaxPivots;   // this warp's staging
+    if (WS) {
+        if (tid == 0) {
+            for (int s2 = 0; s2 < kLazyRing; ++s2)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(fullb + s2)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    unsigned gseq = 0;                                       // ring chunks consumed (scanner warps)
+    auto pbar = [&]() { if (WS) lazy_bar(1, PT); else __syncthreads(); };
     // history: F[t] (m doubles), R[t] (nv doubles), t = 0 .. kLazyMaxPivots-1 (pivot t+1)
     double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)B.gtab_stride;
     double *Rh = Fh + (size_t)kLazyMaxPivots * m;
@@ -165,7 +231,7 @@ lazy_kernel(Batch B) {
             continue;
         }
         // ---- validate (model.py:263-301): every entry of A, streamed once; b above, c below ----
-        if (!B.shared_Ab) {
+        if (!WS && !B.shared_Ab) {
             const size_t total = (size_t)m * n;
             const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;   // 16-byte align the body
             if (tid == 0 && head && total) nonfinite |= !isfinite(Ag[0]);
@@ -192,20 +258,56 @@ lazy_kernel(Batch B) {
             rc[j] = cj;                         // phase 2 runs on c directly (simplex.py:168,180)
             isb[j] = j >= n ? 1 : 0;            // slacks basic
         }
-        const bool invalid = __syncthreads_or(nonfinite);
+        bool invalid = false;
+        if (!WS) invalid = __syncthreads_or(nonfinite);
+        else __syncthreads();
 
         int8_t status = kOptimal;
         int iters = 0;
         double obj = 0.0;
         bool deferred = false;
-        if (invalid) {
-            status = kInvalid;
-        } else {
+        if (WS && tid >= PT) {
+            // scanner warps: A through the bulk-copy ring while the pivot warps solve
+            const int stid = tid - PT;
+            constexpr int ST = 32 * kLazyScanWarps;
+            const size_t total = (size_t)m * n;
+            const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;
+            if (stid == 0 && head && total) nonfinite |= !isfinite(Ag[0]);
+            const size_t nb = total > head ? (total - head) / 2 * 16 : 0;       // 16-byte body
+            const unsigned nch = (unsigned)((nb + kLazyChunk - 1) / kLazyChunk);
+            const char *src = reinterpret_cast<const char *>(Ag + head);
+            auto issue = [&](unsigned c) {
+                const unsigned st = (gseq + c) & (kLazyRing - 1);
+                const size_t off = (size_t)c * kLazyChunk;
+                const unsigned bytes = (unsigned)(nb - off < (size_t)kLazyChunk ? nb - off : (size_t)kLazyChunk);
+                lazy_bulk_load(ring + st * kLazyChunk, src + off, bytes,
+                               (unsigned)__cvta_generic_to_shared(fullb + st));
+            };
+            if (stid == 0)
+                for (unsigned c = 0; c < nch && c < (unsigned)kLazyRing; ++c) issue(c);
+            for (unsigned c = 0; c < nch; ++c) {
+                const unsigned g = gseq + c, st = g & (kLazyRing - 1);
+                lazy_mbar_wait((unsigned)__cvta_generic_to_shared(fullb + st), (g / kLazyRing) & 1);
+                const size_t off = (size_t)c * kLazyChunk;
+                const int len2 = (int)((nb - off < (size_t)kLazyChunk ? nb - off : (size_t)kLazyChunk) / 16);
+                const unsigned buf = ring + st * kLazyChunk;
+#pragma unroll 4
+                for (int q = stid; q < len2; q += ST) {
+                    double x0, x1;
+                    lds_v2_f64(buf + 16u * q, x0, x1);
+                    nonfinite |= !(isfinite(x0) && isfinite(x1));
+                }
+                lazy_bar(2, ST);                              // stage consumed: refill it
+                if (stid == 0 && c + kLazyRing < nch) issue(c + kLazyRing);
+            }
+            gseq += nch;
+            if (stid == 0 && total > head && ((total - head) & 1)) nonfinite |= !isfinite(Ag[total - 1]);
+        } else if (!invalid) {
             // initial entering candidates
             {
                 unsigned long long ck = kKeyEmptyMax;
                 int ci = kNone, cb = kNone;
-                for (int j = tid; j < nv; j += NT) {
+                for (int j = tid; j < nv; j += PT) {
                     if (isb[j]) continue;
                     const unsigned long long k = key_max(rc[j]);
                     if (k > ck || (k == ck && j < ci)) { ck = k; ci = j; }
@@ -216,7 +318,7 @@ lazy_kernel(Batch B) {
                 const int bw = warp_min_int(cb);
                 if (lane == 0) { P->ckey[warp] = kw; P->cidx[warp] = iw; P->cbl[warp] = bw; }
             }
-            __syncthreads();
+            pbar();
             int degenerate_run = 0;
             bool use_bland = false;
             int prev_l = -1, prev_e = -1, prev_old = -1;
@@ -225,7 +327,7 @@ lazy_kernel(Batch B) {
                 // previous pivot's bookkeeping (after the barrier that ended it)
                 if (prev_l >= 0) {
                     if (tid == 0) { basis[prev_l] = prev_e; isb[prev_old] = 0; isb[prev_e] = 1; }
-                    if (tid == (prev_l % NT)) lastpiv[prev_l] = k;
+                    if (tid == (prev_l % PT)) lastpiv[prev_l] = k;
                 }
                 if (k == max_iter) { status = kIterationLimit; iters = max_iter; break; }
                 // choose_entering[_bland] from the warp partials
@@ -245,12 +347,21 @@ lazy_kernel(Batch B) {
                 // entering column by replay (f_i = a_ie before this pivot); ratio test
                 unsigned long long lk = kKeyEmptyMin;
                 int li = kNone;
-                const double *Rcol = Rh + e;
-                for (int i = tid; i < m; i += NT) {
+                if constexpr (RP == 1) {
+                    for (int t = lane; t < k; t += 32) hw[t] = lazy_h(Rh + (size_t)t * nv + e);   // r^t_e
+                    __syncwarp();
+                }
+                for (int i = tid; i < m; i += PT) {
                     const int t0 = lastpiv[i];
-                    double a = t0 ? lazy_h(Rcol + (size_t)(t0 - 1) * nv) : lazy_a0(Ag, n, i, e);
-                    for (int t = t0; t < k; ++t)
-                        a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + i), lazy_h(Rcol + (size_t)t * nv)));
+                    double a;
+                    if constexpr (RP == 1) {
+                        a = t0 ? hw[t0 - 1] : lazy_a0(Ag, n, i, e);
+                        a = lazy_replay(a, Fh + i, (size_t)m, hw, t0, k);
+                    } else {
+                        a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * nv + e) : lazy_a0(Ag, n, i, e);
+                        for (int t = t0; t < k; ++t)
+                            a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + i), lazy_h(Rh + (size_t)t * nv + e)));
+                    }
                     fcur[i] = a;
                     Fh[(size_t)k * m + i] = a;
                     const unsigned long long key = key_min(ratio_entry(rhs[i], a));
@@ -261,7 +372,7 @@ lazy_kernel(Batch B) {
                     const int lw = warp_index_of(lk, kw, li);
                     if (lane == 0) { P->lkey[warp] = kw; P->lrow[warp] = lw; }
                 }
-                __syncthreads();  // S1
+                pbar();  // S1
                 unsigned long long kmin;
                 int l;
                 {
@@ -286,10 +397,19 @@ lazy_kernel(Batch B) {
                 unsigned long long ck = kKeyEmptyMax;
                 int ci = kNone, cb = kNone;
                 double *Rk = Rh + (size_t)k * nv;
-                for (int j = tid; j < nv; j += NT) {
+                if constexpr (RP == 1) {
+                    __syncwarp();
+                    for (int t = t0l + lane; t < k; t += 32) hw[t] = lazy_h(Fh + (size_t)t * m + l);   // f^t_l
+                    __syncwarp();
+                }
+                for (int j = tid; j < nv; j += PT) {
                     double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * nv + j) : lazy_a0(Ag, n, l, j);
-                    for (int t = t0l; t < k; ++t)
-                        a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + l), lazy_h(Rh + (size_t)t * nv + j)));
+                    if constexpr (RP == 1) {
+                        a = lazy_replay(a, Rh + j, (size_t)nv, hw, t0l, k);
+                    } else {
+                        for (int t = t0l; t < k; ++t)
+                            a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + l), lazy_h(Rh + (size_t)t * nv + j)));
+                    }
                     const double r = div_entry(a, pe);
                     Rk[j] = r;
                     const double v = __dsub_rn(rc[j], __dmul_rn(rce, r));
@@ -306,16 +426,25 @@ lazy_kernel(Batch B) {
                     const int bw = warp_min_int(cb);
                     if (lane == 0) { P->ckey[warp] = kw; P->cidx[warp] = iw; P->cbl[warp] = bw; }
                 }
-                for (int i = tid; i < m; i += NT) rhs[i] = i == l ? rrhs : __dsub_rn(rhs[i], __dmul_rn(fcur[i], rrhs));
+                for (int i = tid; i < m; i += PT) rhs[i] = i == l ? rrhs : __dsub_rn(rhs[i], __dmul_rn(fcur[i], rrhs));
                 obj = __dadd_rn(obj, __dmul_rn(rce, rrhs));          // tableau.py:242
                 prev_l = l; prev_e = e; prev_old = oldvar;
-                __syncthreads();  // S3
+                pbar();  // S3
             }
-            __syncthreads();
+            pbar();
             if (prev_l >= 0 && tid == 0) { basis[prev_l] = prev_e; }
-            __syncthreads();
+            pbar();
         }
         (void)obj;
+        if constexpr (WS) {
+            if (tid == 0) { s_res[0] = status; s_res[1] = iters; s_res[2] = deferred; }
+            invalid = __syncthreads_or(nonfinite);           // the stream's verdict joins the solve
+            status = invalid ? (int8_t)kInvalid : (int8_t)s_res[0];
+            iters = invalid ? 0 : s_res[1];
+            deferred = !invalid && s_res[2];
+        } else if (invalid) {
+            status = kInvalid;
+        }
         if (deferred) {
             if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
             __syncthreads();

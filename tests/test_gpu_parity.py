@@ -350,6 +350,40 @@ def test_lazy_disabled_matches_lazy(monkeypatch):
         assert np.array_equal(r1[k], r2[k], equal_nan=True), k
 
 
+@pytest.mark.parametrize("env", [{"BLP_LAZY_WS": "1"}, {"BLP_LAZY_RP": "1"}, {"BLP_LAZY_NT": "256"}])
+def test_lazy_kernel_forms_agree(monkeypatch, env):
+    """The lazy kernel's alternative forms (warp-specialised bulk-copy validation
+    stream, staged replay, CTA size) give the default form's bits, on an odd m*n
+    (LPs alternate between 16-byte aligned and unaligned starts) with non-finite
+    entries at the first and last element of A."""
+    from paper_1802_08557_b200 import _native
+    A, b, c = _single_phase_mix(151, 149, seed=8)
+    A[2, 0, 0] = np.nan
+    A[5, 150, 148] = np.inf
+    A[6, 150, 148] = -np.inf
+    assert _native.kernel_variant(151, 149).startswith("lazy")
+    lim = _native.make_limits()
+    r1 = _native.solve_host(A, b, c, lim)
+    assert (r1["status"][[2, 5, 6]] == 5).all()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r2 = _native.solve_host(A, b, c, lim)
+    for k in r1:
+        assert np.array_equal(r1[k], r2[k], equal_nan=True), k
+
+
+def test_lazy_support_staged_replay_matches_plain(monkeypatch):
+    """Support mode runs the staged replay by default; the plain replay gives the same bits."""
+    from paper_1802_08557_b200 import support_batch, workloads
+    A, b = workloads.support_polytope()
+    C = workloads.support_directions(4096)
+    r1 = _native_dict(support_batch(A, b, C))
+    monkeypatch.setenv("BLP_LAZY_RP", "0")
+    r2 = _native_dict(support_batch(A, b, C))
+    for k in r1:
+        assert np.array_equal(r1[k], r2[k], equal_nan=True), k
+
+
 def test_lazy_path_flags_non_finite_entries():
     """A non-finite entry anywhere in A (found by the concurrent validation pass), b or c
     of a lazy-path batch: that LP comes back BLP_STATUS_INVALID, the others solved."""
