@@ -121,14 +121,23 @@ __device__ __forceinline__ double lazy_h(const double *p) {
 // loaded from p + t*stride (this cell's own history, coalesced across the
 // warp), h the staged broadcast operand.  Loads are issued 8 at a time so a
 // history of k pivots costs k/8 L2 round trips, not k.
-__device__ __forceinline__ double lazy_replay(double a, const double *p, size_t stride, const double *h, int t, int k) {
-    for (; t < k; t += 8) {
+__device__ __forceinline__ double lazy_replay(double a, const double *p, int stride, const double *h, int t, int k) {
+    const double *q = p + (ptrdiff_t)t * stride;
+    for (; t + 8 <= k; t += 8, q += 8 * (ptrdiff_t)stride) {      // full batches: no predicates
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = t + u < k ? lazy_h(p + (size_t)(t + u) * stride) : 0.0;
+        for (int u = 0; u < 8; ++u) v[u] = lazy_h(q + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a = __dsub_rn(a, __dmul_rn(v[u], h[t + u]));
+    }
+    const int rem = k - t;                                            // tail: one predicated batch
+    if (rem > 0) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = u < rem ? lazy_h(q + u * stride) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (t + u < k) a = __dsub_rn(a, __dmul_rn(v[u], h[t + u]));
+            if (u < rem) a = __dsub_rn(a, __dmul_rn(v[u], h[t + u]));
     }
     return a;
 }
@@ -356,7 +365,7 @@ lazy_kernel(Batch B) {
                     double a;
                     if constexpr (RP == 1) {
                         a = t0 ? hw[t0 - 1] : lazy_a0(Ag, n, i, e);
-                        a = lazy_replay(a, Fh + i, (size_t)m, hw, t0, k);
+                        a = lazy_replay(a, Fh + i, m, hw, t0, k);
                     } else {
                         a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * nv + e) : lazy_a0(Ag, n, i, e);
                         for (int t = t0; t < k; ++t)
@@ -405,7 +414,7 @@ lazy_kernel(Batch B) {
                 for (int j = tid; j < nv; j += PT) {
                     double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * nv + j) : lazy_a0(Ag, n, l, j);
                     if constexpr (RP == 1) {
-                        a = lazy_replay(a, Rh + j, (size_t)nv, hw, t0l, k);
+                        a = lazy_replay(a, Rh + j, nv, hw, t0l, k);
                     } else {
                         for (int t = t0l; t < k; ++t)
                             a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + l), lazy_h(Rh + (size_t)t * nv + j)));

@@ -63,8 +63,9 @@ for t in traffic:
 tj = Path("profiles/traffic.json")
 recs = json.loads(tj.read_text()) if tj.exists() else []
 for t in traffic:
+    # one record per (config, LPs, variant): bench.py looks traffic up by variant
     recs = [r for r in recs if not (r["config"] == a.config and r["lps_per_launch"] == a.lps
-                                    and r["kernel"] == t["kernel"])]
+                                    and (r["kernel"] == t["kernel"] or r["variant"] == t["variant_family"]))]
     recs.append(dict(config=a.config, lps_per_launch=a.lps, kernel=t["kernel"], variant=t["variant_family"],
                      dram_bytes_per_launch=t["dram_bytes_per_launch"], source=a.out))
 tj.write_text(json.dumps(recs, indent=1) + "\n")
