@@ -188,7 +188,9 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem)) != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    const long long grid = std::min<long long>((long long)occ * sms, B.count);
+    // BLP_LAZY_PER_SM: cap on resident CTAs per SM (the replay history of all resident CTAs vs L2)
+    const int per_sm = std::max(1, std::min(occ, env_int("BLP_LAZY_PER_SM", occ)));
+    const long long grid = std::min<long long>((long long)per_sm * sms, B.count);
     const long long stride = blp::lazy_scratch_doubles(B.m, B.n);
     // workspace: [0] LP queue, [64] deferred count | defer list | invalid flags | per-CTA replay history
     const size_t list_bytes = ((size_t)B.count * sizeof(int) + 255) / 256 * 256;
