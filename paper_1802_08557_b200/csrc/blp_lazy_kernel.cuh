@@ -247,7 +247,8 @@ lazy_kernel(Batch B) {
             const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
             const size_t n2 = (total - head) / 2;
             size_t q = tid;
-            constexpr int U = LAZY_SCAN_U;         // 16-byte loads in flight per thread
+            // 16-byte loads in flight per thread (C5, 512 threads: 4 -> 5.43 ms, 6 -> 5.22, 8 -> 5.26)
+            constexpr int U = NT >= 512 ? 6 : LAZY_SCAN_U;
             for (; q + (U - 1) * NT < n2; q += U * NT) {
                 double2 v[U];
 #pragma unroll
