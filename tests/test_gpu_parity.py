@@ -350,14 +350,17 @@ def test_lazy_disabled_matches_lazy(monkeypatch):
         assert np.array_equal(r1[k], r2[k], equal_nan=True), k
 
 
-@pytest.mark.parametrize("env", [{"BLP_LAZY_WS": "1"}, {"BLP_LAZY_RP": "1"}, {"BLP_LAZY_NT": "256"}])
+@pytest.mark.parametrize("env", [{"BLP_LAZY_WS": "1"}, {"BLP_LAZY_WS": "1", "BLP_LAZY_PER_SM": "1"},
+                                 {"BLP_LAZY_RP": "1"}, {"BLP_LAZY_NT": "256"}])
 def test_lazy_kernel_forms_agree(monkeypatch, env):
     """The lazy kernel's alternative forms (warp-specialised bulk-copy validation
-    stream, staged replay, CTA size) give the default form's bits, on an odd m*n
+    stream, also with several LPs per CTA so the ring's mbarrier phases carry over
+    between LPs; staged replay; CTA size) give the default form's bits, on an odd m*n
     (LPs alternate between 16-byte aligned and unaligned starts) with non-finite
     entries at the first and last element of A."""
     from paper_1802_08557_b200 import _native
     A, b, c = _single_phase_mix(151, 149, seed=8)
+    A, b, c = np.tile(A, (4, 1, 1)), np.tile(b, (4, 1)), np.tile(c, (4, 1))   # more LPs than CTAs
     A[2, 0, 0] = np.nan
     A[5, 150, 148] = np.inf
     A[6, 150, 148] = -np.inf
