@@ -175,7 +175,18 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
            : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32, 0, 0>
                        : (LazyFn)blp::lazy_kernel<256, 4, 0, 0>;
     const int threads = (nt == 512 || nt == 128 || nt == 64 || nt == 32) ? nt : 256;
-    const size_t smem = blp::lazy_smem_bytes(B.m, B.n, ws_mode, threads, rp);
+    size_t smem = blp::lazy_smem_bytes(B.m, B.n, ws_mode, threads, rp);
+    // BLP_LAZY_FSMEM=1: f^t history of the first pivots in shared memory (two CTAs per SM kept)
+    // (value > 1: per-CTA shared-memory cap in KB; 1: 113 KB)
+    const int fsmem = env_int("BLP_LAZY_FSMEM", 0);
+    if (nt == 512 && !ws_mode && !rp && fsmem) {
+        const size_t base = (smem + 15) / 16 * 16, cap = (size_t)(fsmem > 1 ? fsmem : 113) * 1024;
+        const size_t kf = base < cap ? std::min<size_t>(blp::kLazyMaxPivots, (cap - base) / (8 * (size_t)std::max(1, B.m))) : 0;
+        if (kf >= 4) {
+            fn = (LazyFn)blp::lazy_kernel<512, 2, 0, 0, 1>;
+            smem = base + kf * 8 * (size_t)B.m;
+        }
+    }
     *ws_out = nullptr;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -176,7 +176,10 @@ __device__ __forceinline__ void lazy_bulk_load(unsigned dst, const void *src, un
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
-template <int NT, int MINB, int WS, int RP>
+// FS = 1: the first KF pivots' f^t vectors live in shared memory after the
+// layout (KF from the launch's dynamic shared-memory size), later ones in the
+// L2 scratch.
+template <int NT, int MINB, int WS, int RP, int FS = 0>
 __global__ void __launch_bounds__(NT, MINB)
 lazy_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -211,6 +214,19 @@ lazy_kernel(Batch B) {
     // history: F[t] (m doubles), R[t] (nv doubles), t = 0 .. kLazyMaxPivots-1 (pivot t+1)
     double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)B.gtab_stride;
     double *Rh = Fh + (size_t)kLazyMaxPivots * m;
+    double *Fs = nullptr;
+    int KF = 0;
+    if constexpr (FS) {
+        unsigned dyn;
+        asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        const size_t base = (lazy_smem_bytes(m, n, WS, NT, RP) + 15) / 16 * 16;
+        Fs = reinterpret_cast<double *>(smem + base);
+        KF = (int)min((size_t)kLazyMaxPivots, (dyn - base) / (8 * (size_t)(m > 0 ? m : 1)));
+    }
+    auto Fget = [&](int t, int i) -> double {
+        if constexpr (FS) { if (t < KF) return Fs[(size_t)t * m + i]; }
+        return lazy_h(Fh + (size_t)t * m + i);
+    };
     const int max_iter = B.lim.max_iterations > 0 ? B.lim.max_iterations : 50 * (m + n);
     const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
     const unsigned long long kSent = key_max(kSentinel), kDeg = key_max(kDegenerateTol), kTolK = key_max(kTol);
@@ -370,10 +386,11 @@ lazy_kernel(Batch B) {
                     } else {
                         a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * nv + e) : lazy_a0(Ag, n, i, e);
                         for (int t = t0; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + i), lazy_h(Rh + (size_t)t * nv + e)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), lazy_h(Rh + (size_t)t * nv + e)));
                     }
                     fcur[i] = a;
-                    Fh[(size_t)k * m + i] = a;
+                    if (FS && k < KF) Fs[(size_t)k * m + i] = a;
+                    else Fh[(size_t)k * m + i] = a;
                     const unsigned long long key = key_min(ratio_entry(rhs[i], a));
                     if (key < lk) { lk = key; li = i; }     // rows ascend per thread
                 }
@@ -409,7 +426,7 @@ lazy_kernel(Batch B) {
                 double *Rk = Rh + (size_t)k * nv;
                 if constexpr (RP == 1) {
                     __syncwarp();
-                    for (int t = t0l + lane; t < k; t += 32) hw[t] = lazy_h(Fh + (size_t)t * m + l);   // f^t_l
+                    for (int t = t0l + lane; t < k; t += 32) hw[t] = Fget(t, l);   // f^t_l
                     __syncwarp();
                 }
                 for (int j = tid; j < nv; j += PT) {
@@ -418,7 +435,7 @@ lazy_kernel(Batch B) {
                         a = lazy_replay(a, Rh + j, nv, hw, t0l, k);
                     } else {
                         for (int t = t0l; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(lazy_h(Fh + (size_t)t * m + l), lazy_h(Rh + (size_t)t * nv + j)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), lazy_h(Rh + (size_t)t * nv + j)));
                     }
                     const double r = div_entry(a, pe);
                     Rk[j] = r;

@@ -351,7 +351,7 @@ def test_lazy_disabled_matches_lazy(monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"BLP_LAZY_WS": "1"}, {"BLP_LAZY_WS": "1", "BLP_LAZY_PER_SM": "1"},
-                                 {"BLP_LAZY_RP": "1"}, {"BLP_LAZY_NT": "256"}])
+                                 {"BLP_LAZY_RP": "1"}, {"BLP_LAZY_NT": "256"}, {"BLP_LAZY_FSMEM": "1"}])
 def test_lazy_kernel_forms_agree(monkeypatch, env):
     """The lazy kernel's alternative forms (warp-specialised bulk-copy validation
     stream, also with several LPs per CTA so the ring's mbarrier phases carry over
