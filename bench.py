@@ -12,11 +12,12 @@ data path).  Rank 0 prints one JSON line:
              CUDA events on the launching stream, max over ranks
   e2e        same metric through the public API (batch_solve_arrays) from pinned
              host buffers: H2D of A, b, c + kernels + D2H of every result per step
-  roofline   algorithmic tableau bytes 16(m+1)(n+m+1) per pivot x pivots / kernel
-             time, against the measured smem bandwidth (tableau resident in
-             shared memory) or the measured HBM copy bandwidth (streamed)
+  roofline   the dominant kernel's algorithmic bytes (or flops) / kernel time against
+             the measured peak of the resource that bounds it (roofline_line)
   cpu_baseline  the C oracle port (oracle/, the reference algorithm) on the
              host cores, rank 0 at N=1, on a bounded sample of the workload
+  parity     the timed outputs against the oracle on that sample: status, x,
+             iterations exactly, objective as a true relative error
 
 ``--impl reference`` times that CPU implementation alone (rank 0; other ranks
 exit 0) on the same config and prints the reference arm's line.
@@ -164,8 +165,9 @@ def ncu_traffic(cfg: str, variant: str, count: int):
     return None
 
 
-def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> dict:
-    """The oracle port (reference algorithm in C) on all host cores, bounded sample."""
+def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> tuple[dict, dict]:
+    """The oracle port (reference algorithm in C) on all host cores, bounded sample.
+    Returns (cpu_baseline line, the oracle's outcomes on that sample -- the parity checker)."""
     from oracle import oracle
     cores = oracle.host_cores()
     probe = min(len(c), 2000)
@@ -178,10 +180,29 @@ def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> dict:
     res = oracle.solve_batch(A if shared else A[:sample], b if shared else b[:sample], c[:sample],
                              shared_Ab=shared, threads=cores)
     dt = time.perf_counter() - t0
-    return {"value": sample / dt, "unit": UNIT, "cores": int(res["threads"]), "kind": "port",
+    line = {"value": sample / dt, "unit": UNIT, "cores": int(res["threads"]), "kind": "port",
             "sample": f"first {sample} LPs of this config's rank-0 batch, oracle/blp_oracle.c "
                       f"(full reference tableau incl. artificial columns), {res['threads']} threads, {dt:.2f} s",
             "pivots_per_s": float((res["it1"] + res["it2"]).sum() / dt)}
+    return line, res
+
+
+def parity(got: dict, want: dict) -> dict:
+    """The timed GPU outputs against the oracle on the same LPs (the first len(want) of them):
+    status, x and per-phase iterations exactly; objective as a true relative error."""
+    k = len(want["status"])
+    gs, ws = got["status"][:k], want["status"]
+    opt = (gs == 0) & (ws == 0)
+    x_bad = int((~(got["x"][:k][opt] == want["x"][opt]).all(axis=1)).sum()) if opt.any() else 0
+    go, wo = got["objective"][:k][opt], want["objective"][opt]
+    diff = np.abs(go - wo)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel = np.where(diff == 0, 0.0, diff / np.abs(wo))
+    return {"checked": int(k), "of": int(len(got["status"])), "status_mismatch": int((gs != ws).sum()),
+            "x_mismatch": x_bad,
+            "iter_mismatch": int(((got["it1"][:k] != want["it1"]) | (got["it2"][:k] != want["it2"])).sum()),
+            "max_obj_rel": float(rel.max()) if rel.size else 0.0, "obj_rtol": 1e-9,
+            "checker": "oracle/blp_oracle.c (C restatement of the reference, pinned to tests/golden/)"}
 
 
 def run_reference(args) -> None:
@@ -328,62 +349,24 @@ def main():
     value = total_lps / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel ----
-    # Algorithmic work per pivot: (m+1)(n+m+1) fp64 cells, each read + written
-    # (16 B) and updated by one multiply + one subtract (2 flops) -- BASELINE.md §2.
     variant = _native.kernel_variant(m, n)
-    bpp = bytes_per_pivot(m, n)
-    fpp = 2 * (m + 1) * (n + m + 1)
     secs = step_ms / 1e3
-    achieved_gbs = pivots * bpp / secs / 1e9
-    smem_peak = _native.probe_smem_gbs(local_dev)
-    hbm_peak, hbm_src = measured_hbm_gbs()
-    fp64_peak = _native.probe_fp64_gflops(local_dev) / 1e3
-    # On-chip-resident tableaux (registers or shared memory) are judged against the
-    # measured shared-memory bandwidth, BASELINE.md §2's roofline for C1-C4; the
-    # register variants would only switch to the FP64 bound past 100% of it
-    # (SURVEY.md §8d), so their FP64 fraction is reported alongside.
     input_bytes = (A.nbytes if not shared else 0) + (b.nbytes if not shared else 0) + c.nbytes
     output_bytes = count * (1 + 8 + 8 * n + 4 + 4)
-    lazy_note = None
-    if variant.startswith("lazy"):
-        # The exact lazy tableau (blp_lazy_kernel.cuh) never materialises the dense tableau:
-        # achieved is still SURVEY.md §8(d)'s algorithmic figure (dense-tableau bytes per
-        # pivot x pivots), so frac can exceed 1 -- against HBM when the tableau would not fit
-        # on chip (cluster/hbm shapes), else against shared memory like the dense on-chip
-        # kernels.  inputs_frac = the HBM read of the inputs, the lazy kernel's own floor.
-        if variant.startswith(("lazy+cluster", "lazy+hbm")):
-            bound, unit, achieved, peak, peak_src = "hbm", "GB/s", achieved_gbs, hbm_peak, hbm_src
-        else:
-            bound, unit, achieved, peak = "smem", "GB/s", achieved_gbs, smem_peak
-            peak_src = "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
-        lazy_note = {"inputs_gbs": (input_bytes + output_bytes) / secs / 1e9,
-                     "inputs_frac": (input_bytes + output_bytes) / secs / 1e9 / hbm_peak,
-                     "note": "lazy tableau: frac > 1 means the dense-tableau work was not done "
-                             "(entering column and pivot row recomputed by exact replay); "
-                             "traffic is the DRAM bytes actually moved"}
-    elif variant.startswith(("warplp", "pairlp", "quadlp", "regtile", "smem", "cluster")):
-        bound, unit, achieved, peak = "smem", "GB/s", achieved_gbs, smem_peak
-        peak_src = "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
-    else:
-        bound, unit, achieved, peak = "hbm", "GB/s", achieved_gbs, hbm_peak
-        peak_src = hbm_src
-    traffic = ncu_traffic(args.config, variant, count)
-    roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": variant,
-                "bytes_per_pivot": bpp, "flops_per_pivot": fpp, "pivots_per_launch": pivots,
-                "tableau_gbs": achieved_gbs, "smem_peak_gbs": smem_peak, "smem_frac": achieved_gbs / smem_peak,
-                "hbm_peak_gbs": hbm_peak, "fp64_achieved_tflops": pivots * fpp / secs / 1e12,
-                "fp64_peak_tflops": fp64_peak, "fp64_frac": pivots * fpp / secs / 1e12 / fp64_peak}
-    if lazy_note:
-        roofline.update(lazy_note)
+    roofline = roofline_line(variant, m, n, pivots, secs, input_bytes, output_bytes,
+                             smem_peak=_native.probe_smem_gbs(local_dev),
+                             fp64_peak=_native.probe_fp64_gflops(local_dev) / 1e3,
+                             traffic=ncu_traffic(args.config, variant, count))
 
-    # ---- e2e through the public API from pinned host buffers ----
+    # ---- e2e through the public API from pinned host buffers, on this rank's GPU ----
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     hA, hb, hc = pin(A), pin(b), pin(c)
     h2d = hA.nbytes + hb.nbytes + hc.nbytes
     d2h = count * (1 + 8 + 8 * n + 4 + 4)
     from paper_1802_08557_b200 import support_batch
-    call = (lambda: support_batch(hA, hb, hc)) if shared else (lambda: batch_solve_arrays(hA, hb, hc))
+    devs = (local_dev,)
+    call = (lambda: support_batch(hA, hb, hc, devices=devs)) if shared else \
+        (lambda: batch_solve_arrays(hA, hb, hc, devices=devs))
     call()
     barrier()
     e2e_t = []
@@ -393,17 +376,8 @@ def main():
         r = call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(statistics.median(e2e_t))
-    # PCIe floor for context: one pinned->device copy of this step's inputs
-    tA_h = torch.from_numpy(hA)
-    scratch = torch.empty_like(tA_h, device=dev)
-    torch.cuda.synchronize(dev)
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record()
-    scratch.copy_(tA_h, non_blocking=True)
-    c1.record()
-    torch.cuda.synchronize(dev)
-    h2d_gbs = tA_h.numel() * 8 / (c0.elapsed_time(c1) / 1e3) / 1e9
-    del scratch
+    torch.cuda.set_device(local_dev)
+    h2d_gbs = pinned_h2d_gbs(torch, dev)
     assert np.array_equal(r.status, res["status"]) and np.array_equal(r.x, res["x"]), "e2e result differs"
 
     total_pivots = sum_over_ranks(pivots)
@@ -418,18 +392,94 @@ def main():
         "e2e": {"value": total_lps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                 "h2d_pinned_gbs": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6,
-                "api": "batch_solve_arrays (blp_solve_batch_host: 32 sub-batches pipelined over 4 streams)"},
+                "api": "batch_solve_arrays / support_batch (blp_solve_batch_host: sub-batches pipelined "
+                       "over 4 streams)"},
         "gpu_launches": int(launches),
         "timed_region_ms": region_ms,
         "clocks": clocks.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(A, b, c, shared)
+    # ---- parity of the timed outputs against the oracle (after timing) ----
+    if world == 1:
+        if rank == 0 and not args.no_cpu_baseline:
+            base, want = cpu_baseline(A, b, c, shared)
+            line["cpu_baseline"] = base
+            line["parity"] = parity(res, want)
+    else:
+        # every rank checks a bounded prefix of its own shard; mismatch counts summed over ranks
+        from oracle import oracle
+        k = min(count, 5000)
+        want = oracle.solve_batch(A if shared else A[:k], b if shared else b[:k], c[:k], shared_Ab=shared,
+                                  threads=max(1, oracle.host_cores() // world))
+        pr = parity(res, want)
+        for key in ("checked", "of", "status_mismatch", "x_mismatch", "iter_mismatch"):
+            pr[key] = int(sum_over_ranks(pr[key]))
+        pr["max_obj_rel"] = max_over_ranks(pr["max_obj_rel"])
+        line["parity"] = pr
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def pinned_h2d_gbs(torch, dev, nbytes: int = 512 << 20) -> float:
+    """Pinned host -> device copy rate on a 512 MB buffer (events on an explicit stream of `dev`):
+    the PCIe floor the e2e number is compared with."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    best = 0.0
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            d.copy_(h, non_blocking=True)
+            e1.record(s)
+            s.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
+
+
+def roofline_line(variant: str, m: int, n: int, pivots: int, secs: float, input_bytes: int, output_bytes: int,
+                  *, smem_peak: float, fp64_peak: float, traffic) -> dict:
+    """Roofline of the dominant kernel, with `achieved` always a physical rate of the bound
+    resource (so frac <= 1 up to measurement noise):
+
+    * dense on-chip tableaux (warplp*, pairlp/quadlp, regtile, smem_rpl*, cluster_r*):
+      SURVEY.md §8(d)'s 16(m+1)(n+m+1) B per pivot -- every cell read and written once --
+      against the measured shared-memory bandwidth; FP64 view alongside;
+    * HBM-streamed tableaux (hbm_rpl*): the same bytes against the measured HBM rate;
+    * the exact lazy tableau (lazy+*): the dense tableau is never materialised, so the
+      kernel's algorithmic floor is one HBM read of the inputs plus the outputs, against the
+      measured HBM rate; `dense_equiv_gbs` keeps the §8(d) figure for comparison only.
+    """
+    hbm_peak, hbm_src = measured_hbm_gbs()
+    smem_src = "measured in-run (blp_probe_smem_gbs: LDS.128+STS.128, all SMs)"
+    dense_bpp = bytes_per_pivot(m, n)
+    dense_gbs = pivots * dense_bpp / secs / 1e9
+    fpp = 2 * (m + 1) * (n + m + 1)
+    base = {"kernel": variant, "pivots_per_launch": pivots, "dense_bytes_per_pivot": dense_bpp,
+            "hbm_peak_gbs": hbm_peak, "smem_peak_gbs": smem_peak, "fp64_peak_tflops": fp64_peak}
+    if variant.startswith("lazy"):
+        io = input_bytes + output_bytes
+        achieved = io / secs / 1e9
+        line = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "peak_source": hbm_src, "algorithmic_bytes_per_launch": io,
+                "algorithmic": "inputs read once + outputs written once (the lazy tableau's floor)",
+                "dense_equiv_gbs": dense_gbs}
+        if traffic:
+            line["traffic_over_algorithmic"] = traffic / io
+    elif variant.startswith("hbm"):
+        line = {"bound": "hbm", "achieved": dense_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": dense_gbs / hbm_peak, "traffic": traffic, "peak_source": hbm_src,
+                "bytes_per_pivot": dense_bpp}
+    else:
+        line = {"bound": "smem", "achieved": dense_gbs, "peak": smem_peak, "unit": "GB/s",
+                "frac": dense_gbs / smem_peak, "traffic": traffic, "peak_source": smem_src,
+                "bytes_per_pivot": dense_bpp,
+                "fp64_achieved_tflops": pivots * fpp / secs / 1e12,
+                "fp64_frac": pivots * fpp / secs / 1e12 / fp64_peak}
+    return base | line
 
 
 if __name__ == "__main__":

@@ -407,6 +407,18 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double *sink, int iters
     if (acc == -1.0) sink[0] = acc;
 }
 
+// Restores the caller's current device on every return from a host entry point
+// (they cudaSetDevice to the requested GPU; the caller's torch/CUDA state must not move).
+struct DeviceGuard {
+    int saved = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&saved) != cudaSuccess) { cudaGetLastError(); saved = -1; }
+    }
+    ~DeviceGuard() {
+        if (saved >= 0) cudaSetDevice(saved);
+    }
+};
+
 struct StreamSet {
     std::vector<cudaStream_t> s;
 };
@@ -532,13 +544,33 @@ int solve_host_staged(const double *A, const double *b, const double *c, long lo
         st.in_bytes = in_bytes;
         st.out_bytes = out_bytes;
     }
-    // shared polytope: uploaded once (synchronously), read by every sub-batch
+    // Shared polytope: uploaded once on ss[0] through pinned slot 0 (a pageable source
+    // would let cudaMemcpy return before the DMA lands), and every stream waits for it.
     double *dA_shared = nullptr, *db_shared = nullptr;
     if (shared_Ab) {
         BLP_CUDA_TRY(cudaMalloc(&dA_shared, std::max<size_t>(1, szA) * 8));
         BLP_CUDA_TRY(cudaMalloc(&db_shared, std::max<size_t>(1, szb) * 8));
-        if (szA) BLP_CUDA_TRY(cudaMemcpy(dA_shared, A, szA * 8, cudaMemcpyHostToDevice));
-        if (szb) BLP_CUDA_TRY(cudaMemcpy(db_shared, b, szb * 8, cudaMemcpyHostToDevice));
+        char *hp = nullptr;
+        BLP_CUDA_TRY(cudaMallocHost(reinterpret_cast<void **>(&hp), (szA + szb) * 8 + 16));
+        if (szA) std::memcpy(hp, A, szA * 8);
+        if (szb) std::memcpy(hp + szA * 8, b, szb * 8);
+        cudaError_t e = cudaSuccess;
+        if (szA) e = cudaMemcpyAsync(dA_shared, hp, szA * 8, cudaMemcpyHostToDevice, ss[0]);
+        if (e == cudaSuccess && szb) e = cudaMemcpyAsync(db_shared, hp + szA * 8, szb * 8, cudaMemcpyHostToDevice, ss[0]);
+        cudaEvent_t up;
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming);
+        if (e == cudaSuccess) {
+            e = cudaEventRecord(up, ss[0]);
+            for (int k = 1; k < kSlots && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ss[k], up, 0);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ss[0]);   // hp is freed below
+            cudaEventDestroy(up);
+        }
+        cudaFreeHost(hp);
+        if (e != cudaSuccess) {
+            cudaFree(dA_shared);
+            cudaFree(db_shared);
+            return fail(BLP_ERR_CUDA, std::string("shared polytope upload: ") + cudaGetErrorString(e));
+        }
     }
     cudaEvent_t ev[kSlots];
     for (int k = 0; k < kSlots; ++k) BLP_CUDA_TRY(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
@@ -626,6 +658,7 @@ extern "C" {
 int blp_abi_version(void) { return BLP_ABI_VERSION; }
 
 double blp_probe_fp64_gflops(int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     int sms = 0;
     if (cudaSetDevice(device) != cudaSuccess || device_sms(device, &sms) != BLP_OK) return -1.0;
@@ -651,6 +684,7 @@ double blp_probe_fp64_gflops(int32_t device) {
 }
 
 double blp_probe_smem_gbs(int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     int sms = 0;
     if (cudaSetDevice(device) != cudaSuccess || device_sms(device, &sms) != BLP_OK) return -1.0;
@@ -711,6 +745,7 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
                          int32_t m, int32_t n, int32_t shared_Ab, const blp_limits *limits,
                          int8_t *status, double *objective, double *x, int32_t *iters1,
                          int32_t *iters2, int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     if (bad_args(A, b, c, count, m, n, status, objective, x, iters1, iters2))
         return fail(BLP_ERR_INVALID, "invalid arguments");
@@ -742,18 +777,25 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
     const size_t szA = (size_t)m * n, szb = (size_t)m;
 
     // Shared polytope (support-function mode): one H2D, every stream waits on it.
+    // Errors inside the pipeline break out of it: the streams are always drained and the
+    // shared buffers freed before returning, so no queued D2H can land in the caller's
+    // buffers after this call has returned.
     double *dA_shared = nullptr, *db_shared = nullptr;
     cudaEvent_t shared_ready = nullptr;
-    if (shared_Ab) {
-        BLP_CUDA_TRY(cudaMallocAsync(&dA_shared, std::max<size_t>(1, szA) * sizeof(double), ss[0]));
-        BLP_CUDA_TRY(cudaMallocAsync(&db_shared, std::max<size_t>(1, szb) * sizeof(double), ss[0]));
-        if (szA) BLP_CUDA_TRY(cudaMemcpyAsync(dA_shared, A, szA * sizeof(double), cudaMemcpyHostToDevice, ss[0]));
-        if (szb) BLP_CUDA_TRY(cudaMemcpyAsync(db_shared, b, szb * sizeof(double), cudaMemcpyHostToDevice, ss[0]));
-        BLP_CUDA_TRY(cudaEventCreateWithFlags(&shared_ready, cudaEventDisableTiming));
-        BLP_CUDA_TRY(cudaEventRecord(shared_ready, ss[0]));
-        for (int k = 1; k < kStreams; ++k) BLP_CUDA_TRY(cudaStreamWaitEvent(ss[k], shared_ready, 0));
-    }
     int rc = BLP_OK;
+    auto check = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && rc == BLP_OK) rc = fail(BLP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return rc == BLP_OK;
+    };
+    if (shared_Ab) {
+        check(cudaMallocAsync(&dA_shared, std::max<size_t>(1, szA) * sizeof(double), ss[0]), "cudaMallocAsync");
+        if (rc == BLP_OK) check(cudaMallocAsync(&db_shared, std::max<size_t>(1, szb) * sizeof(double), ss[0]), "cudaMallocAsync");
+        if (rc == BLP_OK && szA) check(cudaMemcpyAsync(dA_shared, A, szA * sizeof(double), cudaMemcpyHostToDevice, ss[0]), "H2D");
+        if (rc == BLP_OK && szb) check(cudaMemcpyAsync(db_shared, b, szb * sizeof(double), cudaMemcpyHostToDevice, ss[0]), "H2D");
+        if (rc == BLP_OK) check(cudaEventCreateWithFlags(&shared_ready, cudaEventDisableTiming), "cudaEventCreate");
+        if (rc == BLP_OK) check(cudaEventRecord(shared_ready, ss[0]), "cudaEventRecord");
+        for (int k = 1; k < kStreams && rc == BLP_OK; ++k) check(cudaStreamWaitEvent(ss[k], shared_ready, 0), "cudaStreamWaitEvent");
+    }
     int ci = 0;
     for (long long start = 0; start < count && rc == BLP_OK; start += chunk, ++ci) {
         const long long cnt = std::min(chunk, count - start);
@@ -761,7 +803,8 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
         const size_t bytes_in = shared_Ab ? (size_t)cnt * n * 8 : (size_t)cnt * (szA + szb + n) * 8;
         const size_t bytes_out = (size_t)cnt * (n * 8 + 8 + 1 + 8) + 64;
         char *buf = nullptr;
-        BLP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes_in + bytes_out + 256, s));
+        if (!check(cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes_in + bytes_out + 256, s), "cudaMallocAsync"))
+            break;
         double *dA = dA_shared, *db = db_shared, *dc;
         char *p = buf;
         if (!shared_Ab) {
@@ -774,37 +817,27 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
         int32_t *dit1 = reinterpret_cast<int32_t *>(p); p += (size_t)cnt * 4;
         int32_t *dit2 = reinterpret_cast<int32_t *>(p); p += (size_t)cnt * 4;
         int8_t *dst = reinterpret_cast<int8_t *>(p);
+        bool ok = true;
         if (!shared_Ab) {
-            if (szA) BLP_CUDA_TRY(cudaMemcpyAsync(dA, A + start * szA, cnt * szA * 8, cudaMemcpyHostToDevice, s));
-            if (szb) BLP_CUDA_TRY(cudaMemcpyAsync(db, b + start * szb, cnt * szb * 8, cudaMemcpyHostToDevice, s));
+            if (szA) ok = check(cudaMemcpyAsync(dA, A + start * szA, cnt * szA * 8, cudaMemcpyHostToDevice, s), "H2D");
+            if (ok && szb) ok = check(cudaMemcpyAsync(db, b + start * szb, cnt * szb * 8, cudaMemcpyHostToDevice, s), "H2D");
         }
-        if (n) BLP_CUDA_TRY(cudaMemcpyAsync(dc, c + start * n, (size_t)cnt * n * 8, cudaMemcpyHostToDevice, s));
-        rc = launch_solve(dA, db, dc, cnt, m, n, shared_Ab, limits, dst, dobj, dx, dit1, dit2, s);
-        if (rc != BLP_OK) break;
-        BLP_CUDA_TRY(cudaMemcpyAsync(status + start, dst, cnt, cudaMemcpyDeviceToHost, s));
-        BLP_CUDA_TRY(cudaMemcpyAsync(objective + start, dobj, cnt * 8, cudaMemcpyDeviceToHost, s));
-        if (n) BLP_CUDA_TRY(cudaMemcpyAsync(x + start * n, dx, (size_t)cnt * n * 8, cudaMemcpyDeviceToHost, s));
-        BLP_CUDA_TRY(cudaMemcpyAsync(iters1 + start, dit1, cnt * 4, cudaMemcpyDeviceToHost, s));
-        BLP_CUDA_TRY(cudaMemcpyAsync(iters2 + start, dit2, cnt * 4, cudaMemcpyDeviceToHost, s));
-        BLP_CUDA_TRY(cudaFreeAsync(buf, s));
-    }
-    if (shared_Ab) {
-        // the last user of the shared polytope may be any stream
-        for (int k = 1; k < kStreams; ++k) {
-            cudaEvent_t ev;
-            BLP_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            BLP_CUDA_TRY(cudaEventRecord(ev, ss[k]));
-            BLP_CUDA_TRY(cudaStreamWaitEvent(ss[0], ev, 0));
-            BLP_CUDA_TRY(cudaEventDestroy(ev));
+        if (ok && n) ok = check(cudaMemcpyAsync(dc, c + start * n, (size_t)cnt * n * 8, cudaMemcpyHostToDevice, s), "H2D");
+        if (ok) {
+            rc = launch_solve(dA, db, dc, cnt, m, n, shared_Ab, limits, dst, dobj, dx, dit1, dit2, s);
+            ok = rc == BLP_OK;
         }
-        BLP_CUDA_TRY(cudaFreeAsync(dA_shared, ss[0]));
-        BLP_CUDA_TRY(cudaFreeAsync(db_shared, ss[0]));
+        if (ok) ok = check(cudaMemcpyAsync(status + start, dst, cnt, cudaMemcpyDeviceToHost, s), "D2H");
+        if (ok) ok = check(cudaMemcpyAsync(objective + start, dobj, cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (ok && n) ok = check(cudaMemcpyAsync(x + start * n, dx, (size_t)cnt * n * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (ok) ok = check(cudaMemcpyAsync(iters1 + start, dit1, cnt * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        if (ok) ok = check(cudaMemcpyAsync(iters2 + start, dit2, cnt * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cudaFreeAsync(buf, s);
     }
-    for (int k = 0; k < kStreams; ++k) {
-        cudaError_t e = cudaStreamSynchronize(ss[k]);
-        if (e != cudaSuccess && rc == BLP_OK)
-            rc = fail(BLP_ERR_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(e));
-    }
+    // drain every stream (also on error), then release the shared polytope
+    for (int k = 0; k < kStreams; ++k) check(cudaStreamSynchronize(ss[k]), "cudaStreamSynchronize");
+    if (dA_shared) cudaFree(dA_shared);
+    if (db_shared) cudaFree(db_shared);
     if (shared_ready) cudaEventDestroy(shared_ready);
     return rc;
 }
@@ -829,6 +862,7 @@ int blp_box_solve_device(const double *lower, const double *upper, const double 
 
 int blp_box_solve_host(const double *lower, const double *upper, const double *direction, int64_t count,
                        int32_t n, double *value, double *point, int32_t *status, int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     if (count < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
     if (count == 0) return BLP_OK;
@@ -899,6 +933,7 @@ int blp_certify_batch_host(const double *A, const double *b, const double *c, co
                            int32_t m, int32_t n, int32_t shared_Ab, const int8_t *status, double tol,
                            double *max_reduced_cost, double *max_violation, double *max_negativity,
                            int8_t *needs_prices, int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     if (count < 0 || m < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
     if (count == 0) return BLP_OK;
@@ -959,6 +994,7 @@ int blp_certify_reprice_device(const double *A, const double *c, const double *y
 int blp_certify_reprice_host(const double *A, const double *c, const double *y, int64_t count, int32_t m,
                              int32_t n, int32_t shared_Ab, const int8_t *mask, double *max_reduced_cost,
                              int32_t device) {
+    DeviceGuard guard;
     g_last_error.clear();
     if (count < 0 || m < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
     if (count == 0) return BLP_OK;

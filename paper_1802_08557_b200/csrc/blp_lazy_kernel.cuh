@@ -511,22 +511,24 @@ lazy_kernel(Batch B) {
 __global__ void __launch_bounds__(256)
 lazy_validate_kernel(const double *A, long long count, long long per_lp, int shared_Ab, unsigned char *flag) {
     const long long total = shared_Ab ? per_lp : count * per_lp;
-    const long long n2 = total / 2;                 // A is 256-byte aligned (cudaMalloc / torch)
-    const double2 *A2 = reinterpret_cast<const double2 *>(A);
+    auto mark = [&](long long e) {
+        if (shared_Ab) { for (long long k = 0; k < count; ++k) flag[k] = 1; }
+        else flag[e / per_lp] = 1;
+    };
+    // A caller's device pointer may be only 8-byte aligned (a torch view A_all[k] with odd
+    // m*n): one scalar head element, then 16-byte loads, then an odd tail element.
+    const long long head = (total > 0 && (reinterpret_cast<uintptr_t>(A) & 15)) ? 1 : 0;
+    const long long n2 = (total - head) / 2;
+    const double2 *A2 = reinterpret_cast<const double2 *>(A + head);
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += stride) {
         const double2 v = __ldcs(A2 + q);
-        if (!isfinite(v.x) || !isfinite(v.y)) {
-            if (shared_Ab) { for (long long k = 0; k < count; ++k) flag[k] = 1; }
-            else {
-                if (!isfinite(v.x)) flag[(2 * q) / per_lp] = 1;
-                if (!isfinite(v.y)) flag[(2 * q + 1) / per_lp] = 1;
-            }
-        }
+        if (!isfinite(v.x)) mark(head + 2 * q);
+        if (!isfinite(v.y)) mark(head + 2 * q + 1);
     }
-    if ((total & 1) && blockIdx.x == 0 && threadIdx.x == 0 && !isfinite(A[total - 1])) {
-        if (shared_Ab) { for (long long k = 0; k < count; ++k) flag[k] = 1; }
-        else flag[(total - 1) / per_lp] = 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (head && !isfinite(A[0])) mark(0);
+        if (((total - head) & 1) && !isfinite(A[total - 1])) mark(total - 1);
     }
 }
 

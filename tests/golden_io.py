@@ -15,6 +15,20 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 OBJ_RTOL = 1e-9   # north star: objective within 1e-9 relative (reference sums c.x with BLAS ddot)
 
 
+def obj_rel_err(got, want) -> np.ndarray:
+    """True relative error |got - want| / |want| (no absolute floor).  A zero reference
+    objective must be matched exactly (rel = inf otherwise, 0 when equal)."""
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    diff = np.abs(got - want)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel = np.where(diff == 0, 0.0, diff / np.abs(want))
+    return rel
+
+
+def obj_close(got, want) -> bool:
+    return bool((obj_rel_err(got, want) <= OBJ_RTOL).all())
+
+
 def _limits(d: dict) -> dict:
     return dict(max_iterations=d["max_iterations"], anti_cycling=d["anti_cycling"],
                 degenerate_pivot_limit=d["degenerate_pivot_limit"])
@@ -69,7 +83,7 @@ def packed_fixture(stem: str) -> dict:
 
 
 def compare(got: dict, want: dict, label: str = "") -> None:
-    """Status, x and iteration counts exactly equal; objective within OBJ_RTOL (relative, floor 1)."""
+    """Status, x and iteration counts exactly equal; objective within OBJ_RTOL (true relative)."""
     gs, ws = np.asarray(got["status"]), np.asarray(want["status"])
     bad = np.flatnonzero(gs != ws)
     assert bad.size == 0, f"{label}: status differs at {bad[:10]} (got {gs[bad[:10]]}, want {ws[bad[:10]]})"
@@ -82,7 +96,7 @@ def compare(got: dict, want: dict, label: str = "") -> None:
     bad = np.flatnonzero(~(gx == wx).all(axis=1)) if gx.size else np.array([], int)
     assert bad.size == 0, f"{label}: x differs on {bad.size} optimal LPs, first {np.flatnonzero(opt)[bad[:5]]}"
     go, wo = np.asarray(got["objective"])[opt], np.asarray(want["objective"])[opt]
-    rel = np.abs(go - wo) / np.maximum(1.0, np.abs(wo))
+    rel = obj_rel_err(go, wo)
     assert (rel <= OBJ_RTOL).all(), f"{label}: objective rel err {rel.max() if rel.size else 0}"
 
 
@@ -116,4 +130,4 @@ def compare_box(value, point, status, rec: dict) -> None:
         return
     assert status == 0, f"{rec['name']}: status {status}"
     assert np.array_equal(np.asarray(point), np.asarray(want["point"])), rec["name"]
-    assert abs(value - want["value"]) <= OBJ_RTOL * max(1.0, abs(want["value"])), rec["name"]
+    assert obj_close(value, want["value"]), rec["name"]

@@ -243,7 +243,7 @@ def test_general_form_batches_match_reference():
     """General-form ingest (MPS fixtures + seeded general LPs) -> packed GPU batches per lowered
     shape -> recover_batch, vs the reference's standardize / solve / recover_outcome."""
     import json
-    from golden_io import GOLDEN, OBJ_RTOL
+    from golden_io import GOLDEN, obj_close
     from paper_1802_08557_b200 import GeneralLP, batch_solve_general, lower_to_general, parse_mps
 
     def glp_of(g):
@@ -269,7 +269,7 @@ def test_general_form_batches_match_reference():
             assert (got.iterations_phase1[k], got.iterations_phase2[k]) == (want["std"]["it1"], want["std"]["it2"]), name
             if w["status"] == 0:
                 assert np.array_equal(got.x[k], np.asarray(w["x"])), name
-                assert abs(got.objective[k] - w["objective"]) <= OBJ_RTOL * max(1.0, abs(w["objective"])), name
+                assert obj_close(got.objective[k], w["objective"]), name
             checked += 1
     assert checked > 650
 
