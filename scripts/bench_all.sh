@@ -2,10 +2,10 @@
 # Bench every BASELINE.json config on one GPU (device-resident value + roofline), JSON lines to gpurun_out/.
 mkdir -p gpurun_out
 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-python bench.py --config c1 --no-cpu-baseline --steps 50 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-python bench.py --config c3 --no-cpu-baseline --steps 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-python bench.py --config c4 --no-cpu-baseline --steps 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-python bench.py --config c5 --no-cpu-baseline --steps 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+python bench.py --config c1 --steps 50 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
+python bench.py --config c3 --steps 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+python bench.py --config c4 --steps 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+python bench.py --config c5 --steps 10 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 for c in c1 c2 c3 c4 c5; do python - "$c" <<'PY'
 import json, sys
 c = sys.argv[1]
@@ -15,7 +15,7 @@ except Exception as e:
     print(c, "FAILED", e); sys.exit()
 r = d["roofline"]
 print(f"{c}: {d['config']['kernel']:16s} value={d['value']:.4g} LPs/s ms={d['ms_per_step']:.3f} "
-      f"roofline {r['bound']} {r['achieved']:.4g}/{r['peak']:.4g} {r['unit']} frac={r['frac']:.3f} "
+      f"roofline {r['bound']} {r['achieved']:.4g}/{r['peak']:.4g} {r['unit']} frac={r["frac"]:.3f} parity={d.get("parity")} "
       f"e2e={d['e2e']['value']:.4g} clocks={d['clocks']['sm_mhz']}")
 PY
 done
