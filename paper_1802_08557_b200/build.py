@@ -17,7 +17,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libblp.so"
-SOURCES = [CSRC / "blp_capi.cu", CSRC / "blp_cluster.cu"]
+SOURCES = [CSRC / "blp_capi.cu", CSRC / "blp_cluster.cu", CSRC / "blp_condensed.cu"]
 OBJDIR = PKG / "build"
 DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "blp.h"]
 

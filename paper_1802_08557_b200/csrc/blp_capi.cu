@@ -24,6 +24,7 @@
 #include "blp_regtile_kernel.cuh"
 #include "blp_warplp_kernel.cuh"
 #include "blp_warplp2_kernel.cuh"
+#include "blp_condensed.h"
 #include "blp_pairlp_kernel.cuh"
 #include "blp_tableau_kernel.cuh"
 #include "blp_box_kernel.cuh"
@@ -169,6 +170,17 @@ bool plan_warplp(int m, int n, Plan *p) {
     return true;
 }
 
+// Condensed-tableau warp-per-LP variants (blp_condensed_kernel.cuh): only the n nonbasic
+// columns + rhs of each row are stored and updated; lane L holds rows L + 32k (k < RPL).
+// BLP_CONDENSED=0 disables the family.
+bool plan_condensed(int m, int n, Plan *p) {
+    if (env_int("BLP_CONDENSED", 1) == 0) return false;
+    blp_condensed::Instance I;
+    if (!blp_condensed::select(m, n, &I)) return false;
+    p->fn = I.fn; p->name = I.name; p->threads = 32; p->smem = I.smem; p->slot = 0;
+    return true;
+}
+
 // Row-warp-per-LP variants (blp_pairlp_kernel.cuh): NWR warps own 32 rows each, a row's
 // first R positions in registers and the next S in a [S][ST] shared tile (ST >= m).
 template <int R, int S, int NWR, int ST, int MINB>
@@ -214,10 +226,11 @@ bool plan_cluster(int m, int n, bool forced, Plan *p) {
     return true;
 }
 
-// BLP_KERNEL=warplp|pairlp|regtile|cluster|smem forces a family (testing / tuning).
+// BLP_KERNEL=condensed|warplp|pairlp|regtile|cluster|smem forces a family (testing / tuning).
 bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
+    if ((any || strcmp(force, "condensed") == 0) && plan_condensed(m, n, p)) return true;
     if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
     bool dense = (any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p);
     if (!dense) {
