@@ -380,6 +380,8 @@ def main():
     h2d_gbs = pinned_h2d_gbs(torch, dev)
     assert np.array_equal(r.status, res["status"]) and np.array_equal(r.x, res["x"]), "e2e result differs"
 
+    obj_api = object_api_e2e(A, b, c, shared, local_dev, res, barrier, max_over_ranks, world, args)
+
     total_pivots = sum_over_ranks(pivots)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -394,6 +396,7 @@ def main():
                 "h2d_pinned_gbs": h2d_gbs, "h2d_floor_ms": h2d / h2d_gbs / 1e6,
                 "api": "batch_solve_arrays / support_batch (blp_solve_batch_host: sub-batches pipelined "
                        "over 4 streams)"},
+        "e2e_object_api": obj_api,
         "gpu_launches": int(launches),
         "timed_region_ms": region_ms,
         "clocks": clocks.summary(),
@@ -420,6 +423,41 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def object_api_e2e(A, b, c, shared, dev: int, res: dict, barrier, max_over_ranks, world: int, args) -> dict:
+    """The reference-facing call itself: batch_solve(list[StandardFormLP], BatchConfig) on
+    this rank's batch (batch.py:134-179), wall clock per call with the list built beforehand
+    (as the reference bench does, cli.py:316-318).  host_marshalling_ms = the C pass over
+    the list (_pyobj.collect) -- the rest of the call is the pipelined gather + H2D +
+    kernels + D2H inside the library, and the lazy outcome list."""
+    from paper_1802_08557_b200 import BatchConfig, StandardFormLP, _pyobj, batch_solve
+    from paper_1802_08557_b200.model import STATUS_BY_CODE
+    count = len(c)
+    lps = [StandardFormLP(c=c[k], A=A if shared else A[k], b=b if shared else b[k]) for k in range(count)]
+    cfg = BatchConfig(devices=(dev,))
+    rep = batch_solve(lps, cfg)
+    times, collect = [], []
+    for _ in range(max(3, min(args.steps, 5))):
+        barrier()
+        t0 = time.perf_counter()
+        _pyobj.collect(lps, b.shape[-1], c.shape[1])
+        collect.append(time.perf_counter() - t0)
+        barrier()
+        t0 = time.perf_counter()
+        rep = batch_solve(lps, cfg)
+        times.append(time.perf_counter() - t0)
+    wall = max_over_ranks(statistics.median(times))
+    want = {STATUS_BY_CODE[int(k)].value: int(v) for k, v in zip(*np.unique(res["status"], return_counts=True))}
+    assert rep.status_counts() == want, "object API result differs"
+    k = int(np.argmax(res["status"] == 0)) if (res["status"] == 0).any() else 0
+    o = rep.outcomes[k]                                   # spot-check one materialised outcome
+    assert o.iterations_phase2 == int(res["it2"][k]) and (o.primal_point is None or
+                                                          np.array_equal(o.primal_point, res["x"][k]))
+    return {"value": count * world / wall, "unit": UNIT, "ms_per_call": wall * 1e3,
+            "host_marshalling_ms": statistics.median(collect) * 1e3, "chunks": rep.plan.count,
+            "api": "batch_solve(list[StandardFormLP], BatchConfig) -> BatchReport "
+                   "(_pyobj.collect + blp_solve_batch_gather; outcomes built on access)"}
 
 
 def pinned_h2d_gbs(torch, dev, nbytes: int = 512 << 20) -> float:

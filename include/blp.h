@@ -101,6 +101,22 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c,
                          int32_t device);
 
 /*
+ * Host batch solve from one pointer per LP array -- the reference's object API
+ * (batch_solve(lps: Sequence[StandardFormLP]), batch.py:134-179) without packing:
+ * A[k] -> that LP's m x n row-major fp64 matrix, b[k] -> m values, c[k] -> n
+ * values (StandardFormLP.A / .b / .c, model.py:103-105).  The library copies
+ * them with host threads straight into its pinned staging ring, overlapped with
+ * the H2D / kernel / D2H of earlier sub-batches; outputs as blp_solve_batch_host.
+ * The caller keeps the arrays alive and unmodified until the call returns.
+ */
+int blp_solve_batch_gather(const double *const *A, const double *const *b, const double *const *c,
+                           int64_t count, int32_t m, int32_t n,
+                           const blp_limits *limits,
+                           int8_t *status, double *objective, double *x,
+                           int32_t *iters1, int32_t *iters2,
+                           int32_t device);
+
+/*
  * Batched hyper-rectangle LPs (the paper's Eq. 7 kernel; reference
  * boxlp.py:44-83 solve_box / solve_box_batch): maximise direction.x over
  * lower <= x <= upper for `count` boxes of dimension n, row-major [count][n].

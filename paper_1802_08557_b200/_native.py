@@ -39,7 +39,7 @@ class Limits(ctypes.Structure):
 _lib = None
 
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
-EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_shape_supported",
+EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_solve_batch_gather", "blp_shape_supported",
            "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
            "blp_probe_smem_gbs", "blp_probe_fp64_gflops", "blp_box_solve_device", "blp_box_solve_host",
            "blp_certify_batch_device", "blp_certify_batch_host", "blp_certify_reprice_device",
@@ -62,6 +62,9 @@ def load():
     lib.blp_solve_batch_device.restype = ctypes.c_int
     lib.blp_solve_batch_host.argtypes = sig + [ctypes.c_int32]
     lib.blp_solve_batch_host.restype = ctypes.c_int
+    lib.blp_solve_batch_gather.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(Limits), P, P, P, P, P, ctypes.c_int32]
+    lib.blp_solve_batch_gather.restype = ctypes.c_int
     lib.blp_shape_supported.argtypes = [ctypes.c_int32, ctypes.c_int32]
     lib.blp_shape_supported.restype = ctypes.c_int
     lib.blp_kernel_variant.argtypes = [ctypes.c_int32, ctypes.c_int32]
@@ -188,6 +191,25 @@ def solve_host(A: np.ndarray, b: np.ndarray, c: np.ndarray, limits: Limits, *, s
     _check(lib.blp_solve_batch_host(_ptr(A), _ptr(b), _ptr(c), count, m, n, 1 if shared_Ab else 0,
                                     ctypes.byref(limits), _ptr(out["status"]), _ptr(out["objective"]),
                                     _ptr(out["x"]), _ptr(out["it1"]), _ptr(out["it2"]), int(device)))
+    return out
+
+
+def solve_gather(ptrs: bytes, count: int, m: int, n: int, limits: Limits, *, device: int = 0,
+                 out: dict | None = None, first: int = 0) -> dict:
+    """One pointer per LP array (blp_solve_batch_gather): `ptrs` is int64[3][total] (A, b, c
+    addresses, _pyobj.collect); LPs [first, first + count) are solved into `out`."""
+    lib = load()
+    _require_gpu()
+    if out is None:
+        out = alloc_outputs(count, n)
+    if count == 0:
+        return out
+    total = len(ptrs) // 24
+    base = ctypes.cast(ctypes.c_char_p(ptrs), ctypes.c_void_p).value
+    pa, pb, pc = (base + 8 * (first + k * total) for k in range(3))
+    _check(lib.blp_solve_batch_gather(pa, pb, pc, count, m, n, ctypes.byref(limits), _ptr(out["status"]),
+                                      _ptr(out["objective"]), _ptr(out["x"]), _ptr(out["it1"]), _ptr(out["it2"]),
+                                      int(device)))
     return out
 
 

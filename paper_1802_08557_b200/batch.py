@@ -24,7 +24,7 @@ import math
 import threading
 import time
 from dataclasses import dataclass, field
-from typing import Sequence
+from collections.abc import Sequence
 
 import numpy as np
 
@@ -90,7 +90,7 @@ class ChunkPlan:
 class BatchReport:
     """Outcomes in input order plus plan and timings (batch.py:77-95)."""
 
-    outcomes: list[SolveOutcome]
+    outcomes: Sequence[SolveOutcome]   # an OutcomeList (list-like, built on access) from batch_solve
     plan: ChunkPlan
     chunk_seconds: list[float]
     total_seconds: float
@@ -102,6 +102,8 @@ class BatchReport:
         return len(self.outcomes) / self.total_seconds
 
     def status_counts(self) -> dict[str, int]:
+        if isinstance(self.outcomes, OutcomeList):
+            return self.outcomes.status_counts()
         counts: dict[str, int] = {}
         for o in self.outcomes:
             counts[o.status.value] = counts.get(o.status.value, 0) + 1
@@ -245,62 +247,149 @@ def _arrays(res: dict) -> BatchArrays:
 # ---------------------------------------------------------------------------
 # reference-compatible object API
 
-def _first_bad_shape(lps: list, m: int, n: int) -> int:
-    """Lowest index whose A is not (m, n), or -1."""
-    for k, lp in enumerate(lps):
+class OutcomeList(Sequence):
+    """``BatchReport.outcomes``: the per-LP ``SolveOutcome``s in input order, built from
+    the packed result arrays when first read (then cached), so a 1e5-LP batch does not
+    pay for 1e5 Python objects it may never look at.  Behaves as the reference's list
+    (batch.py:172): len, indexing, slicing (-> list), iteration, equality with a list."""
+
+    def __init__(self, res: dict):
+        self._res = res
+        self._cache: list[SolveOutcome | None] = [None] * len(res["status"])
+
+    def __len__(self) -> int:
+        return len(self._cache)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError("outcome index out of range")
+        o = self._cache[k]
+        if o is None:
+            o = self._cache[k] = outcome_from_arrays(self._res, k)
+        return o
+
+    def __iter__(self):
+        step = 4096
+        for s0 in range(0, len(self), step):
+            s1 = min(len(self), s0 + step)
+            if any(o is None for o in self._cache[s0:s1]):
+                fresh = outcomes_from_arrays(self._res, s0, s1)
+                for i, o in enumerate(fresh):
+                    if self._cache[s0 + i] is None:
+                        self._cache[s0 + i] = o
+            yield from self._cache[s0:s1]
+
+    def __eq__(self, other):
+        if isinstance(other, (OutcomeList, list, tuple)):
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __repr__(self) -> str:
+        return f"OutcomeList({len(self)} outcomes)"
+
+    def status_counts(self) -> dict[str, int]:
+        """Status.value -> count, keys in first-occurrence order (as the reference's loop)."""
+        codes, first, counts = np.unique(self._res["status"], return_index=True, return_counts=True)
+        order = np.argsort(first, kind="stable")
+        return {STATUS_BY_CODE[int(codes[i])].value: int(counts[i]) for i in order}
+
+
+def _solve_gather_sharded(ptrs: bytes, start: int, end: int, m: int, n: int, limits: SolverLimits,
+                          devices: Sequence[int], out: dict) -> dict:
+    """LPs [start, end) of a pointer table (blp_solve_batch_gather) into out[start:end],
+    contiguous shards over `devices`, one host thread per device."""
+    lim = limits.to_native()
+    count = end - start
+    sub = {k: v[start:end] for k, v in out.items()}
+    devices = list(devices)[:max(1, count)]
+    if len(devices) == 1 or count == 0:
+        if count:
+            _native.solve_gather(ptrs, count, m, n, lim, device=devices[0], out=sub, first=start)
+        return sub
+    errors: list[BaseException] = []
+
+    def work(dev: int, s: int, e: int) -> None:
         try:
-            ok = np.shape(lp.A) == (m, n)
-        except ValueError:  # ragged rows
-            ok = False
-        if not ok:
-            return k
-    return -1
+            _native.solve_gather(ptrs, e - s, m, n, lim, device=dev, out={k: v[s:e] for k, v in sub.items()},
+                                 first=start + s)
+        except BaseException as err:  # re-raised on the caller's thread
+            errors.append(err)
+
+    threads = [threading.Thread(target=work, args=(d, s, e))
+               for d, (s, e) in zip(devices, shard_bounds(count, len(devices)))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return sub
 
 
 def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig()) -> BatchReport:
-    """Solve every LP of a same-shaped batch on the GPU; outcomes land at their input index."""
-    lps = list(lps)
-    shapes = {(lp.m, lp.n) for lp in lps}
-    if len(shapes) > 1:
-        raise HeterogeneousBatch(f"batch mixes LP shapes {sorted(shapes)}")
+    """Solve every LP of a same-shaped batch on the GPU; outcomes land at their input index.
+
+    Marshalling (SURVEY.md §7 hard part iv): one pass in C over the list (_pyobj.collect)
+    takes each LP's A/b/c data pointers and the batch-worst artificial count; the library
+    gathers the arrays with host threads into its pinned staging ring
+    (blp_solve_batch_gather), pipelined with the copies and kernels; outcomes are built
+    lazily (OutcomeList).  LPs whose arrays are not C-contiguous float64 numpy arrays are
+    coerced here first.
+    """
+    from . import _pyobj
+    lps = lps if isinstance(lps, list) else list(lps)
     if not lps:
         return BatchReport(outcomes=[], plan=plan_chunks(0, 1, config), chunk_seconds=[], total_seconds=0.0)
-    m, n = next(iter(shapes))
-    # Pack once, straight into page-locked buffers (the library's H2D copies then run at
-    # full PCIe rate).  The reference raises at the first invalid LP in index order
-    # (validate() inside solve()); a mis-shaped A stops packing there, and non-finite
-    # entries are flagged by the kernel (BLP_STATUS_INVALID).
-    bad_shape = _first_bad_shape(lps, m, n)
-    limit = bad_shape if bad_shape >= 0 else len(lps)
-    A = _native.alloc_host((limit, m, n))
-    b = _native.alloc_host((limit, m))
-    c = _native.alloc_host((limit, n))
-    if limit:
-        np.stack([lp.A for lp in lps[:limit]], out=A)
-        np.stack([lp.b for lp in lps[:limit]], out=b)
-        np.stack([lp.c for lp in lps[:limit]], out=c)
-    # the chunk plan with the batch-worst artificial count (batch.py:146-153), from the packed b
-    worst_artificial = int((b < 0).sum(axis=1).max()) if limit else 0
-    if bad_shape >= 0:
-        worst_artificial = max(worst_artificial, max(int(np.sum(np.asarray(lp.b) < 0)) for lp in lps[limit:]))
+    m, n = lps[0].m, lps[0].n
+    ptrs, slow, worst_artificial, first_hetero = _pyobj.collect(lps, m, n)
+    if first_hetero >= 0:
+        shapes = {(lp.m, lp.n) for lp in lps}
+        raise HeterogeneousBatch(f"batch mixes LP shapes {sorted(shapes)}")
+    count = len(lps)
+    keep = []             # coerced copies of the slow LPs' arrays, alive until the solve returns
+    bad_shape = -1        # the reference raises at the first invalid LP in index order
+    if slow:
+        table = np.frombuffer(ptrs, dtype=np.int64).reshape(3, count).copy()
+        for k in slow:
+            lp = lps[k]
+            worst_artificial = max(worst_artificial, int(np.sum(np.asarray(lp.b, dtype=float) < 0)))
+            if bad_shape >= 0:
+                continue
+            try:
+                ok = np.shape(lp.A) == (m, n)
+            except ValueError:  # ragged rows
+                ok = False
+            if not ok:
+                bad_shape = k
+                continue
+            try:
+                arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in (lp.A, lp.b, lp.c)]
+            except (TypeError, ValueError):   # non-numeric entries: validate() names them
+                bad_shape = k
+                continue
+            keep.append(arrs)
+            table[:, k] = [a.ctypes.data for a in arrs]
+        ptrs = table.tobytes()
     lp_bytes = lp_memory_bytes(m, n, num_slack=m, num_artificial=worst_artificial,
                                data_size_bytes=config.data_size_bytes)
-    plan = plan_chunks(len(lps), lp_bytes, config)
+    plan = plan_chunks(count, lp_bytes, config)
     started = time.perf_counter()        # like batch.py:157, the timer covers everything after planning
+    out = _native.alloc_outputs(count, n)
     if bad_shape >= 0:
         if bad_shape:
-            res = _solve_sharded(A, b, c, config.limits, config.devices, shared_Ab=False)
+            res = _solve_gather_sharded(ptrs, 0, bad_shape, m, n, config.limits, config.devices, out)
             _raise_for_errors(res, lambda k: lps[k])
         raise ValueError(invalid_message(validate(lps[bad_shape])))
-
-    outcomes: list[SolveOutcome | None] = [None] * len(lps)
     chunk_seconds: list[float] = []
     for start, end in plan.bounds:
         t0 = time.perf_counter()
-        res = _solve_sharded(A[start:end], b[start:end], c[start:end], config.limits,
-                             config.devices, shared_Ab=False)
+        res = _solve_gather_sharded(ptrs, start, end, m, n, config.limits, config.devices, out)
         _raise_for_errors(res, lambda k: lps[start + k])
-        outcomes[start:end] = outcomes_from_arrays(res, 0, end - start)
         chunk_seconds.append(time.perf_counter() - t0)
     total = time.perf_counter() - started
-    return BatchReport(outcomes=outcomes, plan=plan, chunk_seconds=chunk_seconds, total_seconds=total)
+    del keep
+    return BatchReport(outcomes=OutcomeList(out), plan=plan, chunk_seconds=chunk_seconds, total_seconds=total)

@@ -43,7 +43,31 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS if p.exists())
 
 
+PYOBJ_SRC = CSRC / "blp_pyobj.c"
+
+
+def pyobj_path() -> Path:
+    import sysconfig
+    return PKG / ("_pyobj" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pyobj(force: bool = False) -> Path:
+    """gcc the CPython marshalling extension (_pyobj: StandardFormLP list -> per-LP pointers)."""
+    import sysconfig
+
+    import numpy
+    out = pyobj_path()
+    if not force and out.exists() and out.stat().st_mtime >= PYOBJ_SRC.stat().st_mtime:
+        return out
+    cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-Wall",
+           "-I" + sysconfig.get_paths()["include"], "-I" + numpy.get_include(),
+           "-o", str(out), str(PYOBJ_SRC)]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_pyobj(force)
     if not force and up_to_date():
         return OUT
     # one object per translation unit, compiled in parallel, then one shared link

@@ -458,6 +458,23 @@ class CopyPool {
         cv_.notify_all();
         for (auto &t : workers_) t.join();
     }
+    // f(0) .. f(parts-1) over the pool (the caller runs f(0)); returns when all are done
+    void parallel_for(int parts, const std::function<void(int)> &f) {
+        parts = std::max(1, std::min(parts, (int)workers_.size() + 1));
+        if (parts == 1) { f(0); return; }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            for (int k = 1; k < parts; ++k) {
+                ++pending_;
+                tasks_.push_back([&f, k] { f(k); });
+            }
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+    int threads() const { return (int)workers_.size() + 1; }
     // memcpy of n bytes split over the pool (and the caller)
     void copy(void *dst, const void *src, size_t n) {
         constexpr size_t kMin = 1 << 20;
@@ -528,10 +545,19 @@ struct Staging {
 Staging g_staging[64];
 std::mutex g_staging_mu[64];
 
+// Where a staged sub-batch's inputs come from: three contiguous packed arrays, or
+// (blp_solve_batch_gather) one pointer per LP for each of A, b, c.
+struct InputSource {
+    const double *A = nullptr, *b = nullptr, *c = nullptr;
+    const double *const *Ap = nullptr, *const *bp = nullptr, *const *cp = nullptr;
+    bool gather() const { return Ap != nullptr; }
+};
+
 // Host-buffer solve through the pinned staging ring (see above).
-int solve_host_staged(const double *A, const double *b, const double *c, long long count, int m, int n,
+int solve_host_staged(const InputSource &src, long long count, int m, int n,
                       int shared_Ab, const blp_limits *lim, int8_t *status, double *objective, double *x,
                       int32_t *it1, int32_t *it2, int device, const std::vector<cudaStream_t> &ss) {
+    const double *A = src.A, *b = src.b, *c = src.c;
     constexpr int kSlots = 4;
     const size_t szA = (size_t)m * n, szb = (size_t)m;
     const size_t in_lp = (shared_Ab ? 0 : (szA + szb) * 8) + (size_t)n * 8;
@@ -615,13 +641,28 @@ int solve_host_staged(const double *A, const double *b, const double *c, long lo
         const long long cnt = std::min(chunk, count - start);
         // stage this sub-batch's inputs: [A][b][c], packed
         char *p = st.in[k];
-        if (!shared_Ab) {
-            if (szA) pool.copy(p, A + start * szA, (size_t)cnt * szA * 8);
-            p += (size_t)cnt * szA * 8;
-            if (szb) pool.copy(p, b + start * szb, (size_t)cnt * szb * 8);
-            p += (size_t)cnt * szb * 8;
+        if (src.gather()) {
+            // one memcpy per LP array, LP ranges split over the copy threads
+            char *pA = p, *pb = p + (size_t)cnt * szA * 8, *pc = pb + (size_t)cnt * szb * 8;
+            const int parts = (int)std::min<long long>(pool.threads(), std::max<long long>(1, cnt / 256));
+            pool.parallel_for(parts, [&](int part) {
+                const long long k0 = cnt * part / parts, k1 = cnt * (part + 1) / parts;
+                for (long long q = k0; q < k1; ++q) {
+                    const long long lpk = start + q;
+                    if (szA) std::memcpy(pA + (size_t)q * szA * 8, src.Ap[lpk], szA * 8);
+                    if (szb) std::memcpy(pb + (size_t)q * szb * 8, src.bp[lpk], szb * 8);
+                    if (n) std::memcpy(pc + (size_t)q * n * 8, src.cp[lpk], (size_t)n * 8);
+                }
+            });
+        } else {
+            if (!shared_Ab) {
+                if (szA) pool.copy(p, A + start * szA, (size_t)cnt * szA * 8);
+                p += (size_t)cnt * szA * 8;
+                if (szb) pool.copy(p, b + start * szb, (size_t)cnt * szb * 8);
+                p += (size_t)cnt * szb * 8;
+            }
+            if (n) pool.copy(p, c + start * n, (size_t)cnt * n * 8);
         }
-        if (n) pool.copy(p, c + start * n, (size_t)cnt * n * 8);
         const size_t bytes_in = (size_t)cnt * in_lp, bytes_out = (size_t)cnt * out_lp;
         char *buf = nullptr;
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes_in + bytes_out + 256, s);
@@ -662,6 +703,17 @@ int solve_host_staged(const double *A, const double *b, const double *c, long lo
     if (dA_shared) cudaFree(dA_shared);
     if (db_shared) cudaFree(db_shared);
     return rc;
+}
+
+// The per-device stream set of the host entry points (created once).
+int device_streams(int device, int count) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto &ss = g_streams[device].s;
+    if (ss.empty()) {
+        ss.resize(count);
+        for (auto &s : ss) BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    }
+    return BLP_OK;
 }
 
 }  // namespace
@@ -767,20 +819,20 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
     BLP_CUDA_TRY(cudaSetDevice(device));
     constexpr int kStreams = 4;
     {
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto &ss = g_streams[device].s;
-        if (ss.empty()) {
-            ss.resize(kStreams);
-            for (auto &s : ss) BLP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        }
+        const int rc = device_streams(device, kStreams);
+        if (rc != BLP_OK) return rc;
     }
     const auto &ss = g_streams[device].s;
     // Pageable caller buffers: through the pinned staging ring (BLP_STAGE=0 disables).
     if (env_int("BLP_STAGE", 1) &&
         !(is_pinned(A) && is_pinned(b) && is_pinned(c) && is_pinned(status) && is_pinned(objective) &&
           is_pinned(x) && is_pinned(iters1) && is_pinned(iters2)))
-        return solve_host_staged(A, b, c, count, m, n, shared_Ab, limits, status, objective, x, iters1, iters2,
+    {
+        InputSource src;
+        src.A = A; src.b = b; src.c = c;
+        return solve_host_staged(src, count, m, n, shared_Ab, limits, status, objective, x, iters1, iters2,
                                  device, ss);
+    }
     // Sub-batches: at least 8192 LPs each, at most 8 of them.
     // Sub-batches: BLP_HOST_CHUNKS of them (default 32), at least 2048 LPs each
     // (measured on C2: 4 -> 17.0 ms, 8 -> 15.5, 16 -> 15.2, 32 -> 14.9, 64 -> 15.2 per 1e5,
@@ -853,6 +905,27 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
     if (db_shared) cudaFree(db_shared);
     if (shared_ready) cudaEventDestroy(shared_ready);
     return rc;
+}
+
+int blp_solve_batch_gather(const double *const *A, const double *const *b, const double *const *c,
+                           int64_t count, int32_t m, int32_t n, const blp_limits *limits, int8_t *status,
+                           double *objective, double *x, int32_t *iters1, int32_t *iters2, int32_t device) {
+    DeviceGuard guard;
+    g_last_error.clear();
+    if (count < 0 || m < 0 || n < 0) return fail(BLP_ERR_INVALID, "invalid arguments");
+    if (count == 0) return BLP_OK;
+    if (!A || !b || !c || !status || !objective || !iters1 || !iters2 || (n > 0 && !x))
+        return fail(BLP_ERR_INVALID, "invalid arguments");
+    for (long long k = 0; k < count; ++k)
+        if ((m && n && !A[k]) || (m && !b[k]) || (n && !c[k])) return fail(BLP_ERR_INVALID, "null LP array pointer");
+    if (device < 0 || device >= 64) return fail(BLP_ERR_INVALID, "device index out of range");
+    BLP_CUDA_TRY(cudaSetDevice(device));
+    const int rc = device_streams(device, 4);
+    if (rc != BLP_OK) return rc;
+    InputSource src;
+    src.Ap = A; src.bp = b; src.cp = c;
+    return solve_host_staged(src, count, m, n, 0, limits, status, objective, x, iters1, iters2, device,
+                             g_streams[device].s);
 }
 
 int blp_box_solve_device(const double *lower, const double *upper, const double *direction, int64_t count,

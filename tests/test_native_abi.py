@@ -38,7 +38,7 @@ def test_host_only_entry_points():
     assert lib.blp_launch_count() >= 0
 
 
-@pytest.mark.parametrize("m,n,family", [(5, 5, "warplp"), (28, 32, "warplp"), (64, 32, "lazy+pairlp"),
+@pytest.mark.parametrize("m,n,family", [(5, 5, "ctab_r1_s8"), (28, 32, "ctab_r1_s32"), (64, 32, "ctab_r2_s32"),
                                         (100, 100, "lazy+quadlp"), (50, 50, "lazy+pairlp"), (100, 150, "lazy+smem"),
                                         (500, 500, "lazy+cluster"),
                                         (150, 150, "lazy+cluster"), (600, 600, "lazy+hbm")])
