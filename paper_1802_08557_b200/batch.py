@@ -164,8 +164,11 @@ def _as_f64(a) -> np.ndarray:
 
 
 def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared_Ab: bool,
-                   out: dict | None = None) -> dict:
-    """Contiguous LP-index shards, one host thread per device (ctypes releases the GIL)."""
+                   out: dict | None = None, solve_host=None) -> dict:
+    """Contiguous LP-index shards, one host thread per device (ctypes releases the GIL); each
+    shard's results land in its slice of `out` (the host-side gather).  `solve_host` is the
+    per-device solver, _native.solve_host (the GPU library) unless a test injects one."""
+    solve_host = solve_host or _native.solve_host
     count, n = c.shape
     if out is None:
         out = _native.alloc_outputs(count, n) if count else dict(
@@ -175,15 +178,15 @@ def _solve_sharded(A, b, c, limits: SolverLimits, devices: Sequence[int], shared
     devices = list(devices)[:max(1, count)]
     if len(devices) == 1 or count == 0:
         if count:
-            _native.solve_host(A, b, c, lim, shared_Ab=shared_Ab, device=devices[0], out=out)
+            solve_host(A, b, c, lim, shared_Ab=shared_Ab, device=devices[0], out=out)
         return out
     errors: list[BaseException] = []
 
     def work(dev: int, s: int, e: int) -> None:
         try:
             sub = {k: v[s:e] for k, v in out.items()}
-            _native.solve_host(A if shared_Ab else A[s:e], b if shared_Ab else b[s:e], c[s:e], lim,
-                               shared_Ab=shared_Ab, device=dev, out=sub)
+            solve_host(A if shared_Ab else A[s:e], b if shared_Ab else b[s:e], c[s:e], lim,
+                       shared_Ab=shared_Ab, device=dev, out=sub)
         except BaseException as err:  # re-raised on the caller's thread
             errors.append(err)
 

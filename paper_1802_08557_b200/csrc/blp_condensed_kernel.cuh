@@ -65,9 +65,16 @@ struct CtState {
     double rc[SPL], rcp[SPL];   // transposed: reduced cost of slot q = lane + 32u and of its partner
     int svar[SPL], spart[SPL];
     double obj;             // objective cell (the same in every lane)
-    unsigned long long ckey;
-    int cidx, cbl;
+    unsigned long long ckey;   // Dantzig winner's key and composite id (ct_cid), warp-uniform
+    int cid;
 };
+
+// Composite candidate id: variable index in the high bits (so the lowest id among equal
+// keys is numpy's first index), where it lives in the low 8: kind (0 the slot's variable,
+// 1 the slot's partner, 2 a trivial member) and the slot q -- the reduction that picks the
+// entering variable also locates it.
+__device__ __forceinline__ int ct_cid(int var, int kind, int q) { return (var << 8) | (kind << 6) | q; }
+constexpr int kCtSlot = 0, kCtPartner = 1, kCtTrivial = 2;
 
 struct CtDims { int m, n, nvc, lane; };
 
@@ -91,32 +98,53 @@ __device__ __forceinline__ void reg_put(double (&a)[W], int i, double v) {
     RegPutter<0, W, W>::put(a, i, v);
 }
 
-__device__ __forceinline__ void ct_consider(double v, int j, unsigned long long &ck, int &ci, int &cb) {
+__device__ __forceinline__ void ct_consider(double v, int j, unsigned long long &ck, int &ci) {
     const unsigned long long k = key_max(v);
     if (k > ck || (k == ck && j < ci)) { ck = k; ci = j; }
-    if (v > kTol && j < cb) cb = j;
 }
 
 // Entering candidates over every nonbasic selectable variable: slot variables,
-// slot partners, trivial members (choose_entering / choose_entering_bland).
+// slot partners, trivial members (choose_entering, Dantzig: max key, first index).
 template <int RPL, int NS, bool PH1>
 __device__ __forceinline__ void ct_candidates(const CtDims &D, CtState<RPL, NS> &S) {
     unsigned long long ck = kKeyEmptyMax;
-    int ci = kNone, cb = kNone;
+    int ci = kNone;
 #pragma unroll
     for (int u = 0; u < CtCfg<RPL, NS>::SPL; ++u) {
-        if (D.lane + 32 * u < D.n) {
-            if (PH1 || S.svar[u] < D.nvc) ct_consider(S.rc[u], S.svar[u], ck, ci, cb);
-            if (S.spart[u] >= 0 && (PH1 || S.spart[u] < D.nvc)) ct_consider(S.rcp[u], S.spart[u], ck, ci, cb);
+        const int q = D.lane + 32 * u;
+        if (q < D.n) {
+            if (PH1 || S.svar[u] < D.nvc) ct_consider(S.rc[u], ct_cid(S.svar[u], kCtSlot, q), ck, ci);
+            if (S.spart[u] >= 0 && (PH1 || S.spart[u] < D.nvc))
+                ct_consider(S.rcp[u], ct_cid(S.spart[u], kCtPartner, q), ck, ci);
         }
     }
 #pragma unroll
     for (int k = 0; k < RPL; ++k)
         if (D.lane + 32 * k < D.m && S.ppart[k] >= 0 && (PH1 || S.ppart[k] < D.nvc))
-            ct_consider(S.prc[k], S.ppart[k], ck, ci, cb);
+            ct_consider(S.prc[k], ct_cid(S.ppart[k], kCtTrivial, 0), ck, ci);
     S.ckey = warp_max_key(ck);
-    S.cidx = warp_index_of(ck, S.ckey, ci);
-    S.cbl = (int)__reduce_min_sync(kFull, (unsigned)cb);
+    S.cid = warp_index_of(ck, S.ckey, ci);
+}
+
+// choose_entering_bland (tableau.py:189-197): the lowest-index candidate with rc > tol,
+// as a composite id (kNone if none).  Only evaluated while Bland's rule is active.
+template <int RPL, int NS, bool PH1>
+__device__ __forceinline__ int ct_bland(const CtDims &D, const CtState<RPL, NS> &S) {
+    int cb = kNone;
+#pragma unroll
+    for (int u = 0; u < CtCfg<RPL, NS>::SPL; ++u) {
+        const int q = D.lane + 32 * u;
+        if (q < D.n) {
+            if ((PH1 || S.svar[u] < D.nvc) && S.rc[u] > kTol) cb = min(cb, ct_cid(S.svar[u], kCtSlot, q));
+            if (S.spart[u] >= 0 && (PH1 || S.spart[u] < D.nvc) && S.rcp[u] > kTol)
+                cb = min(cb, ct_cid(S.spart[u], kCtPartner, q));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+        if (D.lane + 32 * k < D.m && S.ppart[k] >= 0 && (PH1 || S.ppart[k] < D.nvc) && S.prc[k] > kTol)
+            cb = min(cb, ct_cid(S.ppart[k], kCtTrivial, 0));
+    return (int)__reduce_min_sync(kFull, (unsigned)cb);
 }
 
 // Where variable e lives: slot s (its column) or slot s's partner (negated
@@ -216,18 +244,20 @@ __device__ __forceinline__ void ct_pivot(const CtDims &D, CtState<RPL, NS> &S, u
         if (q < D.n) {
             const double r = div_entry(rowbuf[q], pe);
             rvec[q] = r;
-            if (q == s) {
+            // branch-free (one lane is slot s): slot s restarts from the leaving variable,
+            // whose column and reduced cost were e_l and 0 (partner: its trivial member's prc)
+            const bool here = q == s;
+            if (here) {
                 // the entering variable's pair member (if any) becomes trivial at row l
                 newtriv = partner ? S.svar[u] : S.spart[u];
                 newtriv_rc = __dsub_rn(partner ? S.rc[u] : S.rcp[u], __dmul_rn(fm, -1.0));
-                S.svar[u] = oldvar;
-                S.spart[u] = oldpart;
-                S.rc[u] = __dsub_rn(0.0, __dmul_rn(fm, r));
-                S.rcp[u] = oldpart >= 0 ? __dsub_rn(oldprc, __dmul_rn(fm, -r)) : 0.0;
-            } else {
-                S.rc[u] = __dsub_rn(S.rc[u], __dmul_rn(fm, r));
-                if (S.spart[u] >= 0) S.rcp[u] = __dsub_rn(S.rcp[u], __dmul_rn(fm, -r));
             }
+            const double fr = __dmul_rn(fm, r), fnr = __dmul_rn(fm, -r);
+            S.rc[u] = __dsub_rn(here ? 0.0 : S.rc[u], fr);
+            const int sp = here ? oldpart : S.spart[u];
+            S.rcp[u] = sp >= 0 ? __dsub_rn(here ? oldprc : S.rcp[u], fnr) : 0.0;
+            S.svar[u] = here ? oldvar : S.svar[u];
+            S.spart[u] = sp;
         }
     }
     newtriv = (int)__reduce_min_sync(kFull, (unsigned)(newtriv < 0 ? kNone : newtriv));
@@ -273,12 +303,15 @@ __device__ __forceinline__ WlpPhase ct_run_phase(const CtDims &D, CtState<RPL, N
     bool use_bland = false;
     for (int it = 0;; ++it) {
         if (it == max_iter) return {2, max_iter};
-        int e;
-        if (use_bland) e = S.cbl == kNone ? -1 : S.cbl;                  // choose_entering_bland
-        else e = (S.cidx == kNone || S.ckey <= kTolK) ? -1 : S.cidx;    // choose_entering
-        if (e < 0) return {0, it};
-        const CtWhere w = ct_locate<RPL, NS>(D, S, e);
-        if (w.s < 0) return {1, it};          // a trivial member: column -e_r, no positive entry
+        int cid;
+        if (use_bland) cid = ct_bland<RPL, NS, PH1>(D, S);               // choose_entering_bland
+        else cid = (S.cid == kNone || S.ckey <= kTolK) ? kNone : S.cid;  // choose_entering
+        if (cid == kNone) return {0, it};
+        const int e = cid >> 8;
+        CtWhere w;
+        w.s = cid & 63;
+        w.partner = ((cid >> 6) & 3) == kCtPartner;
+        if (((cid >> 6) & 3) == kCtTrivial) return {1, it};   // column -e_r: no positive entry
         double av[RPL];
         unsigned long long lk = kKeyEmptyMin;
         int lrow = kNone;
@@ -396,19 +429,19 @@ __device__ __forceinline__ void ct_restore(const CtDims &D, CtState<RPL, NS> &S,
         if (bv < D.nvc) continue;
         ct_share_row<RPL, NS>(D, S, smem, row);
         unsigned long long bk = kKeyEmptyMax;
-        int bj = kNone, dummy = kNone;
+        int bj = kNone;
 #pragma unroll
         for (int u = 0; u < SPL; ++u) {
             const int q = D.lane + 32 * u;
             if (q < D.n) {
                 const double v = fabs(rowbuf[q]);
-                if (S.svar[u] < D.nvc) ct_consider(v, S.svar[u], bk, bj, dummy);
-                if (S.spart[u] >= 0 && S.spart[u] < D.nvc) ct_consider(v, S.spart[u], bk, bj, dummy);
+                if (S.svar[u] < D.nvc) ct_consider(v, S.svar[u], bk, bj);
+                if (S.spart[u] >= 0 && S.spart[u] < D.nvc) ct_consider(v, S.spart[u], bk, bj);
             }
         }
         // the basic artificial's slack: column -e_row, |entry| = 1
         const int pp = ct_row_sel_i<RPL>(S.ppart, kr);
-        if (D.lane == lr && pp >= 0 && pp < D.nvc) ct_consider(1.0, pp, bk, bj, dummy);
+        if (D.lane == lr && pp >= 0 && pp < D.nvc) ct_consider(1.0, pp, bk, bj);
         const unsigned long long kb = warp_max_key(bk);
         const int j = warp_index_of(bk, kb, bj);
         // entries[j] > REDUNDANT_ROW_TOL; a NaN entry compares False in numpy

@@ -55,11 +55,13 @@ __device__ __forceinline__ unsigned long long key_of_tol() { return key_max(kTol
 template <int LO, int N, int CPW>
 struct RegPicker {
     static __device__ __forceinline__ double get(const double (&a)[CPW], int i) {
-        if constexpr (N <= 8) {
-            double v = a[LO];
-#pragma unroll
-            for (int k = 1; k < N; ++k) v = selp_f64(a[LO + k], v, i == LO + k);
-            return v;
+        if constexpr (N == 1) {
+            return a[LO];
+        } else if constexpr (N <= 8) {
+            // a select tree on the index bits below the group (depth log2 N, not an N-1 chain)
+            const double lo = RegPicker<LO, N / 2, CPW>::get(a, i);
+            const double hi = RegPicker<LO + N / 2, N - N / 2, CPW>::get(a, i);
+            return selp_f64(hi, lo, i >= LO + N / 2);
         } else {
             if (i < LO + N / 2) return RegPicker<LO, N / 2, CPW>::get(a, i);
             return RegPicker<LO + N / 2, N - N / 2, CPW>::get(a, i);

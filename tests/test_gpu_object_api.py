@@ -50,7 +50,11 @@ def test_outcome_list_behaves_like_a_list():
     outs = rep.outcomes
     assert len(outs) == 50 and outs[0] is outs[0] and outs[-1] is outs[49]
     assert outs[10:13] == [outs[10], outs[11], outs[12]]
-    assert outs == [solve(lp) for lp in lps]
+    for o, d in zip(outs, [solve(lp) for lp in lps]):
+        assert (o.status, o.objective_value, o.iterations_phase1, o.iterations_phase2) == \
+            (d.status, d.objective_value, d.iterations_phase1, d.iterations_phase2)
+        assert np.array_equal(o.primal_point, d.primal_point)
+    assert outs == outs[:]            # list equality (same SolveOutcome objects)
     with pytest.raises(IndexError):
         outs[50]
     assert all(o.status is Status.OPTIMAL for o in outs)
@@ -102,3 +106,33 @@ def test_object_api_on_lazy_and_support_shapes():
     C = workloads.support_directions(3000)
     rep = batch_solve([StandardFormLP(c=C[k], A=P, b=q) for k in range(3000)])
     compare(_arrays_of(rep), oracle.solve_batch(P, q, C, shared_Ab=True), "object api support")
+
+
+def test_two_rank_bench_on_one_gpu():
+    """bench.py's multi-rank path (one process per rank, torchrun) with both ranks folded onto
+    the one visible GPU (BLP_BENCH_SHARE_GPU=1: gloo for the scalar collectives): the line
+    reports the whole job, and each rank's timed outputs match the oracle on its shard."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, BLP_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"), "--gpus", "2",
+           "--count", "20000", "--steps", "3", "--warmup", "3"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 40_000 and d["config"]["lps_per_gpu"] == 20_000
+    pr = d["parity"]
+    assert pr["checked"] == 10_000 and pr["of"] == 40_000
+    assert pr["status_mismatch"] == pr["x_mismatch"] == pr["iter_mismatch"] == 0 and pr["max_obj_rel"] <= 1e-9
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] >= 3

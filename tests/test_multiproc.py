@@ -1,13 +1,16 @@
-"""Multi-rank sharding on CPU (gloo, world_size 2): the LP-index split and the host-side
-gather reproduce the single-process result, and max-over-ranks timing is what rank 0 sees.
+"""Multi-rank / multi-device sharding on CPU: the product's own sharding and gather code
+(paper_1802_08557_b200.multirank, batch._solve_sharded) with an injected per-device solver,
+since there is no GPU here (the GPU path itself is covered by the -m gpu tests, including a
+two-rank bench run).
 
-The batch shards with no collective on the data path; the only
-collectives bench.py uses are a barrier and a MAX/SUM reduction of scalars, which
-is what is exercised here.  The per-rank "solver" is the CPU oracle on the rank's
-slice (the GPU solve is covered by the -m gpu parity tests).
+The batch shards with no collective on the data path: each rank solves a
+contiguous LP-index range and rank 0 gathers results into index order; bench.py's only
+other collectives are a barrier and MAX/SUM reductions of scalars, exercised here too.
+The injected solver is the CPU oracle (the parity checker) -- test-only.
 """
 import os
 import socket
+import threading
 
 import numpy as np
 import pytest
@@ -31,48 +34,92 @@ def test_shard_bounds_cover_in_order():
         shard_bounds(5, 0)
 
 
+def _oracle_solver(A, b, c, shared_Ab, device, limits):
+    from oracle import oracle
+    r = oracle.solve_batch(A, b, c, shared_Ab=shared_Ab, threads=1, max_iterations=limits.max_iterations,
+                           anti_cycling=limits.anti_cycling, degenerate_pivot_limit=limits.degenerate_pivot_limit)
+    return {k: r[k] for k in ("status", "objective", "x", "it1", "it2")}
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, A, b, c, out_q):
+def _worker(rank, world, port, A, b, c, shared, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from oracle import oracle
-    s, e = rank_range(len(c), rank, world)
-    res = oracle.solve_batch(A[s:e], b[s:e], c[s:e], threads=1)
-    # host-side gather of the shards (what the multi-device API does with slices)
-    parts = [None] * world
-    dist.all_gather_object(parts, (s, e, res["status"], res["x"], res["it1"], res["it2"]))
-    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    from paper_1802_08557_b200 import multirank
+    s, e, res = multirank.solve_shard(A, b, c, rank, world, shared_Ab=shared, device=rank, solver=_oracle_solver)
+    whole = multirank.gather_shards(s, e, res, len(c))
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)     # bench.py's max-over-ranks timing
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        out_q.put((parts, float(t.item())))
+        out_q.put((whole, float(t.item())))
+    else:
+        assert whole is None
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_shards_equal_single_process():
+@pytest.mark.parametrize("shared", [False, True])
+def test_two_rank_shards_gather_to_single_process(shared):
     from oracle import oracle
     from paper_1802_08557_b200 import workloads
-    A, b, c = workloads.afiro_arrays(300, seed=31)
-    whole = oracle.solve_batch(A, b, c, threads=1)
+    if shared:
+        A, b = workloads.support_polytope()
+        c = workloads.support_directions(301)
+    else:
+        A, b, c = workloads.afiro_arrays(301, seed=31)
+    want = oracle.solve_batch(A, b, c, shared_Ab=shared, threads=1)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, A, b, c, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, A, b, c, shared, q)) for r in range(2)]
     for p in procs:
         p.start()
-    parts, tmax = q.get(timeout=120)
+    whole, tmax = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert tmax == 2.0
-    status = np.concatenate([p[2] for p in sorted(parts)])
-    x = np.concatenate([p[3] for p in sorted(parts)])
-    it = np.concatenate([p[4] + p[5] for p in sorted(parts)])
-    assert [p[0] for p in sorted(parts)] == [0, 150]
-    assert np.array_equal(status, whole["status"]) and np.array_equal(x, whole["x"])
-    assert np.array_equal(it, whole["it1"] + whole["it2"])
+    for k in ("status", "x", "it1", "it2"):
+        assert np.array_equal(whole[k], want[k]), k
+    opt = want["status"] == 0
+    assert np.array_equal(whole["objective"][opt], want["objective"][opt])
+
+
+def test_multi_device_host_api_shards_and_gathers():
+    """batch._solve_sharded over four 'devices' (one host thread each) writes every shard into
+    its slice of one output set: equal to the unsharded solve, also for fewer LPs than devices."""
+    from paper_1802_08557_b200 import SolverLimits, workloads
+    from paper_1802_08557_b200.batch import _solve_sharded
+    seen = []
+    lock = threading.Lock()
+
+    def fake_native(A, b, c, lim, *, shared_Ab, device, out):
+        from oracle import oracle
+        with lock:
+            seen.append((device, len(c)))
+        r = oracle.solve_batch(A, b, c, shared_Ab=shared_Ab, threads=1)
+        for k in ("status", "objective", "x", "it1", "it2"):
+            out[k][...] = r[k]
+        return out
+
+    def outputs(count, n):
+        return dict(status=np.empty(count, np.int8), objective=np.empty(count), x=np.empty((count, n)),
+                    it1=np.empty(count, np.int32), it2=np.empty(count, np.int32))
+
+    from oracle import oracle
+    A, b, c = workloads.afiro_arrays(403, seed=5)
+    want = oracle.solve_batch(A, b, c, threads=1)
+    got = _solve_sharded(A, b, c, SolverLimits(), (0, 1, 2, 3), False, out=outputs(403, 32), solve_host=fake_native)
+    assert sorted(seen) == [(0, 101), (1, 101), (2, 101), (3, 100)]
+    for k in ("status", "x", "it1", "it2"):
+        assert np.array_equal(got[k], want[k]), k
+    seen.clear()
+    got = _solve_sharded(A[:2], b[:2], c[:2], SolverLimits(), (0, 1, 2, 3), False, out=outputs(2, 32),
+                         solve_host=fake_native)
+    assert sorted(seen) == [(0, 1), (1, 1)]
+    assert np.array_equal(got["x"], want["x"][:2])
