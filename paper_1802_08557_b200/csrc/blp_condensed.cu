@@ -11,7 +11,8 @@ namespace blp_condensed {
 
 namespace {
 struct Row { int rpl, ns; Instance inst; };
-// kMinBlocks = resident LPs per SM the register budget is tuned for
+// kMinBlocks = resident LPs per SM the register budget is tuned for (C2, ctab_r1_s32:
+// 16 -> 128 registers, 5.05 ms per 1e5; 20 -> 96 registers + spills, 6.37 ms)
 const Row kInstances[] = {
     {1, 8, {blp::condensed_kernel<1, 8, 24>, "ctab_r1_s8", blp::CtCfg<1, 8>::BYTES}},
     {1, 16, {blp::condensed_kernel<1, 16, 20>, "ctab_r1_s16", blp::CtCfg<1, 16>::BYTES}},
@@ -24,30 +25,12 @@ const Row kInstances[] = {
     {4, 16, {blp::condensed_kernel<4, 16, 8>, "ctab_r4_s16", blp::CtCfg<4, 16>::BYTES}},
 };
 
-// Occupancy alternatives (BLP_CT_OCC=1): the same shapes tuned for more resident LPs
-// per SM at the cost of a few spilled registers.
-const Row kDense[] = {
-    {1, 32, {blp::condensed_kernel<1, 32, 20>, "ctab_r1_s32_o20", blp::CtCfg<1, 32>::BYTES}},
-};
-
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-}
-
 int rows_per_lane(int m) { return m <= 32 ? 1 : (m <= 64 ? 2 : (m <= 128 ? 4 : 0)); }
 }  // namespace
 
 bool select(int m, int n, Instance *out) {
     if (m < 1 || n < 1) return false;
     const int rpl = rows_per_lane(m);
-    if (env_int("BLP_CT_OCC", 0)) {
-        for (const Row &r : kDense) {
-            if (r.rpl != rpl || n > r.ns || n <= r.ns / 2) continue;
-            *out = r.inst;
-            return true;
-        }
-    }
     for (const Row &r : kInstances) {
         if (r.rpl != rpl || n > r.ns) continue;
         *out = r.inst;
