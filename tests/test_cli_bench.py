@@ -50,4 +50,4 @@ def test_bench_small_cell_schema_and_counts(capsys):
     counts = batch_solve(gen_random_lps(4, 8, seed=5), BatchConfig()).status_counts()
     assert int(f["n_optimal"]) == counts.get("optimal", 0)
     assert int(f["n_infeasible"]) == counts.get("infeasible", 0)
-    assert f["kernel"].startswith("warplp")
+    assert f["kernel"].startswith(("ctab", "warplp"))
