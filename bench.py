@@ -48,7 +48,7 @@ def parse_args():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "c4b", "c5b"])
     p.add_argument("--count", type=int, default=None, help="LPs per GPU (default: the config's size)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -74,6 +74,13 @@ def workload(cfg: str, count: int | None, rank: int):
         A, b = workloads.support_polytope()
         c = workloads.support_directions(cnt, offset=rank * cnt)
         shared = True
+    elif cfg == "c4b":
+        A, b = workloads.support_polytope_two_phase()
+        c = workloads.support_directions(cnt, offset=rank * cnt)
+        shared = True
+    elif cfg == "c5b":
+        A, b, c = workloads.big_two_phase_arrays(cnt, seed=55 + 1000 * rank)
+        shared = False
     else:
         A, b, c = workloads.random_arrays(500, cnt, 5 + 1000 * rank)
         shared = False
@@ -515,10 +522,11 @@ def roofline_line(variant: str, m: int, n: int, pivots: int, secs: float, input_
                 "dense_equiv_gbs": dense_gbs}
         if traffic:
             line["traffic_over_algorithmic"] = traffic / io
-    elif variant.startswith("ctab"):
-        # condensed tableau (blp_condensed_kernel.cuh): only the (m+1) x (n+1) nonbasic + rhs
-        # cells exist, in registers -- no tableau byte crosses shared memory or HBM, so the
-        # physical resource the update consumes is the FP64 pipe: one DMUL + one DADD per cell
+    elif variant.startswith(("ctab", "cm")):
+        # condensed tableau (blp_condensed_kernel.cuh, blp_cmulti_kernel.cuh): only the
+        # (m+1) x (n+1) nonbasic + rhs cells exist, in registers (cm*: a few slots per row in a
+        # shared tile) -- the physical resource the update consumes is the FP64 pipe: one
+        # DMUL + one DADD per cell
         cfp = 2 * (m + 1) * (n + 1)
         fl = pivots * cfp / secs / 1e12
         line = {"bound": "fp64", "achieved": fl, "peak": fp64_peak, "unit": "TFLOP/s", "frac": fl / fp64_peak,

@@ -61,6 +61,8 @@ struct Plan {
     long long slot = 0;  // doubles of global tableau per CTA (HBM-streamed variant)
     bool lazy = false;     // the exact lazy-tableau kernel runs first; this one takes its deferred LPs
     bool cluster = false;  // cluster-resident variant (blp_cluster.cu): launched by blp_cluster::launch
+    blp_condensed::Phase1Fn phase1 = nullptr;   // condensed: shared phase-1 prologue (support mode)
+    size_t p1_bytes = 0;
 };
 
 int env_int(const char *name, int dflt) {
@@ -177,7 +179,8 @@ bool plan_condensed(int m, int n, Plan *p) {
     if (env_int("BLP_CONDENSED", 1) == 0) return false;
     blp_condensed::Instance I;
     if (!blp_condensed::select(m, n, &I)) return false;
-    p->fn = I.fn; p->name = I.name; p->threads = 32; p->smem = I.smem; p->slot = 0;
+    p->fn = I.fn; p->name = I.name; p->threads = I.threads; p->smem = I.smem; p->slot = 0;
+    p->phase1 = I.phase1; p->p1_bytes = I.p1_bytes;
     return true;
 }
 
@@ -230,7 +233,18 @@ bool plan_cluster(int m, int n, bool forced, Plan *p) {
 bool plan_launch(int m, int n, Plan *p) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
-    if ((any || strcmp(force, "condensed") == 0) && plan_condensed(m, n, p)) return true;
+    if ((any || strcmp(force, "condensed") == 0) && plan_condensed(m, n, p)) {
+        // the multi-warp condensed form (33..128 rows) takes the lazy kernel's deferrals, as
+        // the dense 33..128-row kernels do (below)
+        p->lazy = p->threads > 32 && any && m > 32 && env_int("BLP_LAZY_SMALL", 1) != 0 &&
+                  blp_cluster::lazy_enabled(m, n);
+        if (p->lazy) {
+            static thread_local std::string cname;
+            cname = std::string("lazy+") + p->name;
+            p->name = cname.c_str();
+        }
+        return true;
+    }
     if ((any || strcmp(force, "warplp") == 0) && plan_warplp(m, n, p)) return true;
     bool dense = (any || strcmp(force, "pairlp") == 0) && plan_pairlp(m, n, p);
     if (!dense) {
@@ -290,6 +304,7 @@ void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c
     B.gtab_stride = 0;
     B.defer_list = nullptr;
     B.defer_count = nullptr;
+    B.p1state = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -343,7 +358,9 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
 
-    const size_t ws_bytes = 256 + (size_t)P.slot * sizeof(double) * (size_t)grid;
+    const size_t slot_bytes = (size_t)P.slot * sizeof(double) * (size_t)grid;
+    const bool p1 = shared_Ab && P.phase1 != nullptr;
+    const size_t ws_bytes = 256 + slot_bytes + (p1 ? P.p1_bytes : 0);
     void *ws = nullptr;
     BLP_CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, stream));
     BLP_CUDA_TRY(cudaMemsetAsync(ws, 0, 256, stream));
@@ -356,11 +373,20 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.gtab_stride = P.slot;
     B.defer_list = defer_list;
     B.defer_count = defer_count;
+    B.p1state = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
     B.lim.reserved = 0;
 
+    if (p1) {   // support mode: phase 1 + restore_objective once for the shared A, b
+        double *st = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256 + slot_bytes);
+        BLP_CUDA_TRY(cudaFuncSetAttribute(P.phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+        P.phase1<<<1, 32, P.smem, stream>>>(B, st);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        BLP_CUDA_TRY(cudaGetLastError());
+        B.p1state = st;
+    }
     P.fn<<<(unsigned)grid, P.threads, P.smem, stream>>>(B);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     BLP_CUDA_TRY(cudaGetLastError());

@@ -65,6 +65,9 @@ struct Batch {
     // exactly those (*defer_count of them, read on the device).
     int *defer_list;
     int *defer_count;
+    // Shared phase 1 (support mode, condensed kernels): the restored post-phase-1 tableau
+    // and its status, written once per batch by condensed_phase1_kernel; null otherwise.
+    const double *p1state;
 };
 
 // Number of LPs a kernel launch processes, and the batch index of its k-th.

@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 
+#include "blp_cmulti_kernel.cuh"
 #include "blp_condensed_kernel.cuh"
 
 namespace blp_condensed {
@@ -14,22 +15,66 @@ struct Row { int rpl, ns; Instance inst; };
 // kMinBlocks = resident LPs per SM the register budget is tuned for (C2, ctab_r1_s32:
 // 16 -> 128 registers, 5.05 ms per 1e5; 20 -> 96 registers + spills, 6.37 ms)
 const Row kInstances[] = {
-    {1, 8, {blp::condensed_kernel<1, 8, 24>, "ctab_r1_s8", blp::CtCfg<1, 8>::BYTES}},
-    {1, 16, {blp::condensed_kernel<1, 16, 20>, "ctab_r1_s16", blp::CtCfg<1, 16>::BYTES}},
-    {1, 32, {blp::condensed_kernel<1, 32, 16>, "ctab_r1_s32", blp::CtCfg<1, 32>::BYTES}},
-    {1, 64, {blp::condensed_kernel<1, 64, 8>, "ctab_r1_s64", blp::CtCfg<1, 64>::BYTES}},
-    {2, 8, {blp::condensed_kernel<2, 8, 12>, "ctab_r2_s8", blp::CtCfg<2, 8>::BYTES}},
-    {2, 16, {blp::condensed_kernel<2, 16, 10>, "ctab_r2_s16", blp::CtCfg<2, 16>::BYTES}},
-    {2, 32, {blp::condensed_kernel<2, 32, 8>, "ctab_r2_s32", blp::CtCfg<2, 32>::BYTES}},
-    {4, 8, {blp::condensed_kernel<4, 8, 10>, "ctab_r4_s8", blp::CtCfg<4, 8>::BYTES}},
-    {4, 16, {blp::condensed_kernel<4, 16, 8>, "ctab_r4_s16", blp::CtCfg<4, 16>::BYTES}},
+    {1, 8, {blp::condensed_kernel<1, 8, 24>, "ctab_r1_s8", blp::CtCfg<1, 8>::BYTES,
+              blp::condensed_phase1_kernel<1, 8>, blp::CtP1<1, 8>::BYTES}},
+    {1, 16, {blp::condensed_kernel<1, 16, 20>, "ctab_r1_s16", blp::CtCfg<1, 16>::BYTES,
+              blp::condensed_phase1_kernel<1, 16>, blp::CtP1<1, 16>::BYTES}},
+    {1, 32, {blp::condensed_kernel<1, 32, 16>, "ctab_r1_s32", blp::CtCfg<1, 32>::BYTES,
+              blp::condensed_phase1_kernel<1, 32>, blp::CtP1<1, 32>::BYTES}},
+    {1, 64, {blp::condensed_kernel<1, 64, 8>, "ctab_r1_s64", blp::CtCfg<1, 64>::BYTES,
+              blp::condensed_phase1_kernel<1, 64>, blp::CtP1<1, 64>::BYTES}},
+    {2, 8, {blp::condensed_kernel<2, 8, 12>, "ctab_r2_s8", blp::CtCfg<2, 8>::BYTES,
+              blp::condensed_phase1_kernel<2, 8>, blp::CtP1<2, 8>::BYTES}},
+    {2, 16, {blp::condensed_kernel<2, 16, 10>, "ctab_r2_s16", blp::CtCfg<2, 16>::BYTES,
+              blp::condensed_phase1_kernel<2, 16>, blp::CtP1<2, 16>::BYTES}},
+    {2, 32, {blp::condensed_kernel<2, 32, 8>, "ctab_r2_s32", blp::CtCfg<2, 32>::BYTES,
+              blp::condensed_phase1_kernel<2, 32>, blp::CtP1<2, 32>::BYTES}},
+    {4, 8, {blp::condensed_kernel<4, 8, 10>, "ctab_r4_s8", blp::CtCfg<4, 8>::BYTES,
+              blp::condensed_phase1_kernel<4, 8>, blp::CtP1<4, 8>::BYTES}},
+    {4, 16, {blp::condensed_kernel<4, 16, 8>, "ctab_r4_s16", blp::CtCfg<4, 16>::BYTES,
+              blp::condensed_phase1_kernel<4, 16>, blp::CtP1<4, 16>::BYTES}},
 };
+
+// Multi-warp condensed form (blp_cmulti_kernel.cuh): NWR row-warps, R register slots and S
+// tile slots per row, tile stride ST (odd, >= m), kMinBlocks LPs per SM.
+struct MRow { int nwr, ns; Instance inst; };
+#define CM_INST(NWR, R, S, ST, MB)                                                                     \
+    {NWR, R + S, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
+                  blp::CmCfg<NWR, R, S, ST>::BYTES, nullptr, 0, 32 * NWR}}
+const MRow kMulti[] = {
+    CM_INST(2, 32, 0, 65, 8),
+    CM_INST(2, 64, 0, 65, 4),
+    CM_INST(4, 32, 0, 129, 4),
+    CM_INST(4, 48, 16, 129, 3),
+    CM_INST(4, 88, 16, 129, 2),
+    CM_INST(4, 96, 32, 129, 2),
+};
+#undef CM_INST
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
 
 int rows_per_lane(int m) { return m <= 32 ? 1 : (m <= 64 ? 2 : (m <= 128 ? 4 : 0)); }
 }  // namespace
 
 bool select(int m, int n, Instance *out) {
     if (m < 1 || n < 1) return false;
+    // BLP_CMULTI: 0 never, 1 (default) for 65..128 rows and where the one-warp form has no
+    // instance, 2 for every 33..128-row shape
+    const int cm = env_int("BLP_CMULTI", 1);
+    if (m > 32 && m <= 128 && cm != 0) {
+        const int nwr = m <= 64 ? 2 : 4;
+        const bool one_warp_fits = (m <= 64 && n <= 32) || (m > 64 && n <= 16);
+        if (cm == 2 || m > 64 || !one_warp_fits) {
+            for (const MRow &r : kMulti) {
+                if (r.nwr != nwr || n > r.ns) continue;
+                *out = r.inst;
+                return true;
+            }
+        }
+    }
     const int rpl = rows_per_lane(m);
     for (const Row &r : kInstances) {
         if (r.rpl != rpl || n > r.ns) continue;

@@ -477,6 +477,158 @@ __device__ __forceinline__ void ct_restore(const CtDims &D, CtState<RPL, NS> &S,
     }
 }
 
+// build_tableau (tableau.py:139-172): rows straight into their lane, validation fused
+// (a non-finite A, b or c entry sets `nonfinite`); slot q starts as structural x_q with
+// reduced cost c_q (0 without c: the shared phase-1 prologue).  Returns n_art.
+template <int RPL, int NS>
+__device__ __forceinline__ int ct_build(const CtDims &D, CtState<RPL, NS> &S, const double *Ag, const double *bg,
+                                        const double *cg, bool &nonfinite) {
+    constexpr int SPL = CtCfg<RPL, NS>::SPL;
+    const int m = D.m, n = D.n, nvc = D.nvc;
+    unsigned negm[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+        const int row = D.lane + 32 * k;
+        const bool live = row < m;
+        const double bi = live ? bg[row] : 0.0;
+        nonfinite |= !isfinite(bi);
+        const bool neg = live && bi < 0.0;
+        negm[k] = __ballot_sync(kFull, neg);
+        const double sgn = neg ? -1.0 : 1.0;
+        S.rhs[k] = live ? __dmul_rn(bi, sgn) : 0.0;
+        const double *arow = Ag + (size_t)(live ? row : 0) * n;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+            double v = 0.0;
+            if (live && c < n) {
+                const double x = arow[c];
+                nonfinite |= !isfinite(x);
+                v = __dmul_rn(x, sgn);
+            }
+            S.a[k][c] = v;
+        }
+    }
+    int n_art = 0;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+        const int row = D.lane + 32 * k;
+        const bool neg = (negm[k] >> D.lane) & 1u;
+        const int art = n_art + __popc(negm[k] & ((1u << D.lane) - 1u));
+        S.basis[k] = neg ? nvc + art : n + row;
+        S.ppart[k] = neg ? n + row : -1;      // the negated row's slack: column -e_row
+        S.prc[k] = 0.0;
+        n_art += __popc(negm[k]);
+    }
+#pragma unroll
+    for (int u = 0; u < SPL; ++u) {
+        const int q = D.lane + 32 * u;
+        S.svar[u] = q;                         // slot q: structural x_q
+        S.spart[u] = -1;
+        S.rc[u] = (cg && q < n) ? cg[q] : 0.0;
+        S.rcp[u] = 0.0;
+        if (cg && q < n) nonfinite |= !isfinite(S.rc[u]);
+    }
+    S.obj = 0.0;
+    return n_art;
+}
+
+// Phase 1 (simplex.py:168-178): build_auxiliary, _run_phase, the infeasibility test and
+// restore_objective.  c-independent: the objective is -1 on the artificials.  Returns
+// the status if the LP ends here (else kOptimal) and the phase-1 iterations in it1.
+template <int RPL, int NS>
+__device__ __forceinline__ int ct_phase1(const CtDims &D, CtState<RPL, NS> &S, unsigned char *smem,
+                                         const Limits &lim, int &it1) {
+    ct_price_out<RPL, NS, true>(D, S, smem, nullptr);
+    const WlpPhase p1 = ct_run_phase<RPL, NS, true>(D, S, smem, lim);
+    it1 = p1.iters;
+    if (p1.state == 2) return kIterationLimit;
+    if (p1.state == 1) return kErrPhase1Unbounded;
+    if (fabs(S.obj) > kPhase1ZeroTol) return kInfeasible;
+    ct_restore<RPL, NS>(D, S, smem);
+    return kOptimal;
+}
+
+// Shared phase 1 (support-function mode, one A and b for every direction): phase 1 and
+// restore_objective depend only on A and b, so the prologue runs them
+// once and every direction starts from the restored condensed tableau (L2-resident, read
+// coalesced: field-major, lane-minor) with its own price-out of c.
+template <int RPL, int NS>
+struct CtP1 {
+    static constexpr int SPL = CtCfg<RPL, NS>::SPL;
+    static constexpr int ND = RPL * NS + 2 * RPL;          // a, rhs, prc
+    static constexpr int NI = 2 * RPL + 2 * SPL;           // basis, ppart, svar, spart
+    static constexpr size_t BYTES = 32 * (ND * 8 + NI * 4) + 16;
+    // info (4 ints after the state): [0] status of phase 1 (kOptimal = continue),
+    // [1] phase-1 iterations, [2] mode (0: no b < 0 -- directions build as usual, 1: shared)
+};
+
+template <int RPL, int NS>
+__device__ __forceinline__ void ct_dump(const CtDims &D, const CtState<RPL, NS> &S, double *st) {
+    using P = CtP1<RPL, NS>;
+    int *si = reinterpret_cast<int *>(st + 32 * P::ND);
+    const int l = D.lane;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+#pragma unroll
+        for (int c = 0; c < NS; ++c) st[(k * NS + c) * 32 + l] = S.a[k][c];
+        st[(RPL * NS + k) * 32 + l] = S.rhs[k];
+        st[(RPL * NS + RPL + k) * 32 + l] = S.prc[k];
+        si[k * 32 + l] = S.basis[k];
+        si[(RPL + k) * 32 + l] = S.ppart[k];
+    }
+#pragma unroll
+    for (int u = 0; u < P::SPL; ++u) {
+        si[(2 * RPL + u) * 32 + l] = S.svar[u];
+        si[(2 * RPL + P::SPL + u) * 32 + l] = S.spart[u];
+    }
+}
+
+template <int RPL, int NS>
+__device__ __forceinline__ void ct_load(const CtDims &D, CtState<RPL, NS> &S, const double *st) {
+    using P = CtP1<RPL, NS>;
+    const int *si = reinterpret_cast<const int *>(st + 32 * P::ND);
+    const int l = D.lane;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+#pragma unroll
+        for (int c = 0; c < NS; ++c) S.a[k][c] = st[(k * NS + c) * 32 + l];
+        S.rhs[k] = st[(RPL * NS + k) * 32 + l];
+        S.prc[k] = st[(RPL * NS + RPL + k) * 32 + l];
+        S.basis[k] = si[k * 32 + l];
+        S.ppart[k] = si[(RPL + k) * 32 + l];
+    }
+#pragma unroll
+    for (int u = 0; u < P::SPL; ++u) {
+        S.svar[u] = si[(2 * RPL + u) * 32 + l];
+        S.spart[u] = si[(2 * RPL + P::SPL + u) * 32 + l];
+    }
+    S.obj = 0.0;
+}
+
+// One warp: the shared polytope's phase 1 into `st` (support mode only).
+template <int RPL, int NS>
+__global__ void __launch_bounds__(32, 1) condensed_phase1_kernel(Batch B, double *st) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using C = CtCfg<RPL, NS>;
+    int *info = reinterpret_cast<int *>(st + 32 * CtP1<RPL, NS>::ND) + 32 * CtP1<RPL, NS>::NI;
+    CtDims D;
+    D.m = B.m; D.n = B.n; D.nvc = B.n + B.m; D.lane = threadIdx.x;
+    for (int q = D.lane; q < NS; q += 32) reinterpret_cast<double *>(smem + C::RVEC)[q] = 0.0;
+    CtState<RPL, NS> S;
+    bool nonfinite = false;
+    const int n_art = ct_build<RPL, NS>(D, S, B.A, B.b, nullptr, nonfinite);
+    const bool invalid = __any_sync(kFull, nonfinite);
+    int status = kOptimal, it1 = 0;
+    if (invalid) status = kInvalid;
+    else if (n_art > 0) status = ct_phase1<RPL, NS>(D, S, smem, B.lim, it1);
+    ct_dump<RPL, NS>(D, S, st);
+    if (D.lane == 0) {
+        info[0] = status;
+        info[1] = it1;
+        info[2] = (invalid || n_art > 0) ? 1 : 0;
+    }
+}
+
 template <int RPL, int NS, int kMinBlocks>
 __global__ void __launch_bounds__(32, kMinBlocks)
 condensed_kernel(Batch B) {
@@ -485,7 +637,7 @@ condensed_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
     CtDims D;
     D.m = B.m; D.n = B.n; D.nvc = B.n + B.m; D.lane = threadIdx.x;
-    const int m = D.m, n = D.n, nvc = D.nvc;
+    const int m = D.m, n = D.n;
     {
         double *rvec = reinterpret_cast<double *>(smem + C::RVEC);
         for (int q = D.lane; q < NS; q += 32) rvec[q] = 0.0;   // unused slots read as 0
@@ -504,73 +656,44 @@ condensed_kernel(Batch B) {
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;
 
-        // ---- build_tableau (tableau.py:139-172): rows straight into their lane; validation fused ----
-        bool nonfinite = false;
-        unsigned negm[RPL];
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-            const int row = D.lane + 32 * k;
-            const bool live = row < m;
-            const double bi = live ? bg[row] : 0.0;
-            nonfinite |= !isfinite(bi);
-            const bool neg = live && bi < 0.0;
-            negm[k] = __ballot_sync(kFull, neg);
-            const double sgn = neg ? -1.0 : 1.0;
-            S.rhs[k] = live ? __dmul_rn(bi, sgn) : 0.0;
-            const double *arow = Ag + (size_t)(live ? row : 0) * n;
-#pragma unroll
-            for (int c = 0; c < NS; ++c) {
-                double v = 0.0;
-                if (live && c < n) {
-                    const double x = arow[c];
-                    nonfinite |= !isfinite(x);
-                    v = __dmul_rn(x, sgn);
-                }
-                S.a[k][c] = v;
-            }
-        }
-        int n_art = 0;
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) {
-            const int row = D.lane + 32 * k;
-            const bool neg = (negm[k] >> D.lane) & 1u;
-            const int art = n_art + __popc(negm[k] & ((1u << D.lane) - 1u));
-            S.basis[k] = neg ? nvc + art : n + row;
-            S.ppart[k] = neg ? n + row : -1;      // the negated row's slack: column -e_row
-            S.prc[k] = 0.0;
-            n_art += __popc(negm[k]);
-        }
-#pragma unroll
-        for (int u = 0; u < SPL; ++u) {
-            const int q = D.lane + 32 * u;
-            S.svar[u] = q;                         // slot q: structural x_q
-            S.spart[u] = -1;
-            S.rc[u] = q < n ? cg[q] : 0.0;
-            S.rcp[u] = 0.0;
-            if (q < n) nonfinite |= !isfinite(S.rc[u]);
-        }
-        S.obj = 0.0;
-        const bool invalid = __any_sync(kFull, nonfinite);
-
         int8_t status = kOptimal;
         int it1 = 0, it2 = 0;
         bool done = false;
-        if (invalid) {
-            status = kInvalid;
-            done = true;
-        } else if (n_art > 0) {
-            ct_price_out<RPL, NS, true>(D, S, smem, cg);                 // build_auxiliary
-            const WlpPhase p1 = ct_run_phase<RPL, NS, true>(D, S, smem, B.lim);
-            it1 = p1.iters;
-            if (p1.state == 2) { status = kIterationLimit; done = true; }
-            else if (p1.state == 1) { status = kErrPhase1Unbounded; done = true; }
-            else if (fabs(S.obj) > kPhase1ZeroTol) { status = kInfeasible; done = true; }
-            else {
-                ct_restore<RPL, NS>(D, S, smem);
+        // support mode with b < 0: phase 1 was solved once by condensed_phase1_kernel (its info
+        // block is re-read per LP -- an L1 hit -- rather than held in registers across the solve)
+        const int *p1info = B.p1state ? reinterpret_cast<const int *>(B.p1state + 32 * CtP1<RPL, NS>::ND) +
+                                        32 * CtP1<RPL, NS>::NI : nullptr;
+        if (p1info && p1info[2] == 1) {
+            const int p1status = p1info[0], p1iters = p1info[1];
+            bool nonfinite = false;
+#pragma unroll
+            for (int u = 0; u < SPL; ++u)
+                if (D.lane + 32 * u < n) nonfinite |= !isfinite(cg[D.lane + 32 * u]);
+            if (__any_sync(kFull, nonfinite) || p1status == kInvalid) {
+                status = kInvalid;
+                done = true;
+            } else if (p1status != kOptimal) {
+                status = (int8_t)p1status;
+                it1 = p1iters;
+                done = true;
+            } else {
+                it1 = p1iters;
+                ct_load<RPL, NS>(D, S, B.p1state);
                 ct_price_out<RPL, NS, false>(D, S, smem, cg);
             }
         } else {
-            ct_candidates<RPL, NS, false>(D, S);
+            bool nonfinite = false;
+            const int n_art = ct_build<RPL, NS>(D, S, Ag, bg, cg, nonfinite);
+            if (__any_sync(kFull, nonfinite)) {
+                status = kInvalid;
+                done = true;
+            } else if (n_art > 0) {
+                const int st = ct_phase1<RPL, NS>(D, S, smem, B.lim, it1);
+                if (st != kOptimal) { status = (int8_t)st; done = true; }
+                else ct_price_out<RPL, NS, false>(D, S, smem, cg);
+            } else {
+                ct_candidates<RPL, NS, false>(D, S);
+            }
         }
         if (!done) {
             const WlpPhase p2 = ct_run_phase<RPL, NS, false>(D, S, smem, B.lim);

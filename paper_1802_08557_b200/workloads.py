@@ -136,6 +136,28 @@ def support_polytope(seed: int = 4, m: int = 64, n: int = 32):
     return A, b
 
 
+def support_polytope_two_phase(seed: int = 44, m: int = 64, n: int = 32, lower: int = 16):
+    """C4b: the C4 polytope with `lower` lower-bound rows, so b has negative entries and every
+    direction needs phase 1 -- the same phase 1 for all of them.
+
+    Draw order: A ~ U(-1,1) [m,n]; b ~ U(1,2) [m]; t ~ U(0.01,0.02) [lower].  Then A[:n] += 2I;
+    rows n..n+lower-1 become -e_k (k < lower) with b = -t_k (x_k >= t_k); the last row is all
+    ones with b = 1e3.  x = 0.02 on the first `lower` coordinates (0 elsewhere) is feasible.
+    """
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1.0, 1.0, size=(m, n))
+    b = rng.uniform(1.0, 2.0, size=m)
+    t = rng.uniform(0.01, 0.02, size=lower)
+    A[:n] += 2.0 * np.eye(n)
+    for k in range(lower):
+        A[n + k] = 0.0
+        A[n + k, k] = -1.0
+        b[n + k] = -t[k]
+    A[m - 1] = 1.0
+    b[m - 1] = 1e3
+    return A, b
+
+
 def support_directions(count: int = 1_000_000, seed: int = 4, n: int = 32, offset: int = 0):
     """C4 directions: C ~ N(0,1) [count, n], drawn after the polytope from the same seed."""
     rng = np.random.default_rng(seed)
@@ -162,6 +184,10 @@ CONFIGS = {
     "c3": dict(m=100, n=100, count=100_000, doc="100x100 degenerate mix + Bland, seed 3"),
     "c4": dict(m=64, n=32, count=1_000_000, doc="support function: one 64x32 polytope, 1e6 directions, seed 4"),
     "c5": dict(m=500, n=500, count=10_000, doc="gen_random_lps(500, 1e4, seed=5), 4 MB tableaux (cluster-resident)"),
+    # stress variants (not BASELINE.json configs): C4 with a shared phase 1, C5 two-phase
+    "c4b": dict(m=64, n=32, count=1_000_000,
+                doc="support function, two-phase: 64x32 polytope with 16 b < 0 rows (seed 44), 1e6 directions"),
+    "c5b": dict(m=500, n=500, count=8, doc="C2 recipe at 500x500, seed 55 (two-phase, ~12k pivots per LP)"),
 }
 
 
@@ -183,5 +209,11 @@ def make_config(name: str, count: int | None = None, offset: int = 0):
         return A, b, support_directions(cnt, offset=offset), True
     if name == "c5":
         A, b, c = big_arrays(cnt)
+        return A, b, c, False
+    if name == "c4b":
+        A, b = support_polytope_two_phase()
+        return A, b, support_directions(cnt, offset=offset), True
+    if name == "c5b":
+        A, b, c = big_two_phase_arrays(cnt)
         return A, b, c, False
     raise KeyError(name)

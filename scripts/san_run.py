@@ -22,7 +22,11 @@ CASES = {
     "warplp2_c2": ("afiro:28:32:64", {"BLP_CONDENSED": "0"}),
     "warplp_c1": ("random:5:64", {"BLP_CONDENSED": "0"}),
     "pairlp_c4": ("afiro:64:32:24", {"BLP_CONDENSED": "0", "BLP_LAZY_SMALL": "0"}),
-    "quadlp_c3": ("c3:8", {"BLP_LAZY_SMALL": "0"}),
+    "quadlp_c3": ("c3:8", {"BLP_LAZY_SMALL": "0", "BLP_CMULTI": "0"}),
+    "cmulti_c3": ("c3:8", {"BLP_LAZY_SMALL": "0"}),
+    "cmulti_lazy_c3": ("c3:8", {}),
+    "cmulti_c4": ("afiro:64:32:24", {"BLP_CMULTI": "2", "BLP_LAZY_SMALL": "0"}),
+    "condensed_p1": ("support2:64", {}),
     "lazy_c3": ("random:100:12", {}),
     "lazy_support": ("support:64", {"BLP_CONDENSED": "0"}),
     "lazy_150": ("random:150:6", {}),
@@ -43,6 +47,9 @@ def make(spec: str):
         return (*workloads.random_arrays(dim, cnt, seed=12), False)
     if kind == "c3":
         return (*workloads.degenerate_arrays(int(a[0]), seed=3), False)
+    if kind == "support2":
+        A, b = workloads.support_polytope_two_phase()
+        return A, b, workloads.support_directions(int(a[0])), True
     if kind == "support":
         A, b = workloads.support_polytope()
         return A, b, workloads.support_directions(int(a[0])), True

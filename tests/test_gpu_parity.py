@@ -210,7 +210,8 @@ def test_box_batch_1e5_against_oracle():
 
 
 FAMILY_SHAPES = [(3, 5), (12, 19), (28, 32), (30, 31), (31, 32), (32, 32), (33, 20), (40, 50), (64, 33),
-                 (64, 34), (65, 8), (100, 100), (128, 73), (128, 74), (90, 140)]
+                 (64, 34), (65, 8), (100, 100), (128, 73), (128, 74), (90, 140), (100, 60), (120, 110),
+                 (70, 128), (128, 128)]
 
 
 @pytest.mark.parametrize("m,n", FAMILY_SHAPES)
@@ -225,10 +226,11 @@ def test_every_kernel_family_matches_oracle(m, n, monkeypatch):
     A, b, c = (np.concatenate(v) for v in ((A1, A2), (b1, b2), (c1, c2)))
     want = oracle.solve_batch(A, b, c)
     seen = set()
-    for force, hbm in (("", "0"), ("warplp", "0"), ("pairlp", "0"), ("regtile", "0"), ("smem", "0"),
-                       ("smem", "1")):
+    for force, hbm, cm in (("", "0", "1"), ("condensed", "0", "0"), ("condensed", "0", "2"), ("warplp", "0", "1"),
+                           ("pairlp", "0", "1"), ("regtile", "0", "1"), ("smem", "0", "1"), ("smem", "1", "1")):
         monkeypatch.setenv("BLP_KERNEL", force)
         monkeypatch.setenv("BLP_FORCE_HBM", hbm)
+        monkeypatch.setenv("BLP_CMULTI", cm)
         variant = _native.kernel_variant(m, n)
         if variant in seen:
             continue
