@@ -26,6 +26,7 @@
 #include "blp_common.cuh"
 #include "blp_condensed_kernel.cuh"
 #include "blp_keys.cuh"
+#include "blp_pairlp_kernel.cuh"
 
 namespace blp {
 
@@ -210,13 +211,9 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
             St.a[c] = __dsub_rn(St.a[c], __dmul_rn(av, r2.x));
             St.a[c + 1] = __dsub_rn(St.a[c + 1], __dmul_rn(av, r2.y));
         }
-        if (!mine) {
-#pragma unroll
-            for (int c = 0; c < S; ++c) {
-                double *t = tile + (size_t)c * ST + D.row;
-                *t = __dsub_rn(*t, __dmul_rn(av, rvec[R + c]));
-            }
-        }
+        // tile slots: software-pipelined (the tile and rvec share the shared-memory array, so
+        // plain loads would serialise behind the previous column's store); row l: r - 0*r, as numpy
+        if constexpr (S > 0) pair_update_tile<R, S, ST>(tile + D.row, rvec, mine ? 0.0 : av);
     }
     if ((l >> 5) == D.warp) {        // numpy: r - 0*r == r; warp-uniform reload of row l
         const unsigned rv = (unsigned)__cvta_generic_to_shared(rvec);

@@ -37,17 +37,23 @@ const Row kInstances[] = {
 
 // Multi-warp condensed form (blp_cmulti_kernel.cuh): NWR row-warps, R register slots and S
 // tile slots per row, tile stride ST (odd, >= m), kMinBlocks LPs per SM.
-struct MRow { int nwr, ns; Instance inst; };
+struct MRow { int nwr, ns, r; Instance inst; };
 #define CM_INST(NWR, R, S, ST, MB)                                                                     \
-    {NWR, R + S, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
+    {NWR, R + S, R, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
                   blp::CmCfg<NWR, R, S, ST>::BYTES, nullptr, 0, 32 * NWR}}
+// First fit in this order.  C3 (100 x 100, c3 count 2e4, device-resident): r48_s56 at 3 LPs
+// per SM 74.8 ms; r88_s16 (2 per SM) 88.0; r80_s24 89.5; r64_s40 94.7; r96_s32 107.7.
 const MRow kMulti[] = {
     CM_INST(2, 32, 0, 65, 8),
     CM_INST(2, 64, 0, 65, 4),
     CM_INST(4, 32, 0, 129, 4),
     CM_INST(4, 48, 16, 129, 3),
-    CM_INST(4, 88, 16, 129, 2),
+    CM_INST(4, 48, 56, 129, 3),
     CM_INST(4, 96, 32, 129, 2),
+    // A/B alternatives (BLP_CM_R selects the register width)
+    CM_INST(4, 88, 16, 129, 2),
+    CM_INST(4, 80, 24, 129, 2),
+    CM_INST(4, 64, 40, 129, 2),
 };
 #undef CM_INST
 
@@ -68,8 +74,10 @@ bool select(int m, int n, Instance *out) {
         const int nwr = m <= 64 ? 2 : 4;
         const bool one_warp_fits = (m <= 64 && n <= 32) || (m > 64 && n <= 16);
         if (cm == 2 || m > 64 || !one_warp_fits) {
+            const int want_r = env_int("BLP_CM_R", 0);
             for (const MRow &r : kMulti) {
                 if (r.nwr != nwr || n > r.ns) continue;
+                if (want_r && r.r != want_r) continue;
                 *out = r.inst;
                 return true;
             }

@@ -255,6 +255,31 @@ lazy_kernel(Batch B) {
             __syncthreads();
             continue;
         }
+        // ---- validate (model.py:263-301): every entry of A, streamed once; b above, c below ----
+        // (Measured, not kept: the stream after the solve, so the solve's reads of A are still in
+        // L2 when it passes them -- 1.1 GB less DRAM per C5 launch but 5.18 -> 5.36 ms.)
+        if (!WS && !B.shared_Ab) {
+            const size_t total = (size_t)m * n;
+            const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;   // 16-byte align the body
+            if (tid == 0 && head && total) nonfinite |= !isfinite(Ag[0]);
+            const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
+            const size_t n2 = (total - head) / 2;
+            size_t q = tid;
+            // 16-byte loads in flight per thread (C5, 512 threads: 4 -> 5.43 ms, 6 -> 5.22, 8 -> 5.26)
+            constexpr int U = NT >= 512 ? 6 : LAZY_SCAN_U;
+            for (; q + (U - 1) * NT < n2; q += U * NT) {
+                double2 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = lazy_scan_load(A2 + q + u * NT);
+#pragma unroll
+                for (int u = 0; u < U; ++u) nonfinite |= !(isfinite(v[u].x) && isfinite(v[u].y));
+            }
+            for (; q < n2; q += NT) {
+                const double2 v = __ldcs(A2 + q);
+                nonfinite |= !(isfinite(v.x) && isfinite(v.y));
+            }
+            if (tid == 0 && ((total - head) & 1)) nonfinite |= !isfinite(Ag[total - 1]);
+        }
         for (int j = tid; j < nv; j += NT) {
             const double cj = j < n ? cg[j] : 0.0;
             nonfinite |= !isfinite(cj);
@@ -456,35 +481,6 @@ lazy_kernel(Batch B) {
             if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
             __syncthreads();
             continue;
-        }
-        // ---- validate (model.py:263-301): every entry of A, streamed once (b and c were checked
-        // before the solve).  After the solve, not before: the solve's reads of A (entering-column
-        // sectors of row-major A, pivot rows) are then still in L2 when the stream passes them,
-        // instead of being fetched from DRAM a second time.  A non-finite entry cannot hang the
-        // solve (the pivot budget bounds it) and turns its result into BLP_STATUS_INVALID.
-        if (!WS && !B.shared_Ab && !invalid) {
-            const size_t total = (size_t)m * n;
-            const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;   // 16-byte align the body
-            bool nfa = false;
-            if (tid == 0 && head && total) nfa |= !isfinite(Ag[0]);
-            const double2 *A2 = reinterpret_cast<const double2 *>(Ag + head);
-            const size_t n2 = (total - head) / 2;
-            size_t q = tid;
-            // 16-byte loads in flight per thread (C5, 512 threads: 4 -> 5.43 ms, 6 -> 5.22, 8 -> 5.26)
-            constexpr int U = NT >= 512 ? 6 : LAZY_SCAN_U;
-            for (; q + (U - 1) * NT < n2; q += U * NT) {
-                double2 v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) v[u] = lazy_scan_load(A2 + q + u * NT);
-#pragma unroll
-                for (int u = 0; u < U; ++u) nfa |= !(isfinite(v[u].x) && isfinite(v[u].y));
-            }
-            for (; q < n2; q += NT) {
-                const double2 v = __ldcs(A2 + q);
-                nfa |= !(isfinite(v.x) && isfinite(v.y));
-            }
-            if (tid == 0 && ((total - head) & 1)) nfa |= !isfinite(Ag[total - 1]);
-            if (__syncthreads_or(nfa)) { status = kInvalid; iters = 0; }
         }
         // ---- _extract_point (simplex.py:146-151) and c @ x ----
         double *xs = fcur;                       // reuse: n <= ? -> write x straight to global

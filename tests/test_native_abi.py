@@ -39,7 +39,7 @@ def test_host_only_entry_points():
 
 
 @pytest.mark.parametrize("m,n,family", [(5, 5, "ctab_r1_s8"), (28, 32, "ctab_r1_s32"), (64, 32, "ctab_r2_s32"),
-                                        (100, 100, "lazy+cm4_r88_s16"), (50, 50, "lazy+cm2_r64_s0"), (100, 150, "lazy+smem"),
+                                        (100, 100, "lazy+cm4_r48_s56"), (50, 50, "lazy+cm2_r64_s0"), (100, 150, "lazy+smem"),
                                         (90, 140, "lazy+smem"), (64, 40, "lazy+cm2_r64_s0"),
                                         (500, 500, "lazy+cluster"),
                                         (150, 150, "lazy+cluster"), (600, 600, "lazy+hbm")])
