@@ -356,7 +356,7 @@ def main():
     value = total_lps / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel ----
-    variant = _native.kernel_variant(m, n)
+    variant = _native.kernel_variant(m, n, shared)
     secs = step_ms / 1e3
     if variant.startswith("lazy+"):
         # the lazy tableau hands phase-1 LPs (b < 0) and LPs past its pivot budget to the dense

@@ -172,6 +172,9 @@ int blp_shape_supported(int32_t m, int32_t n);
 /* Name of the kernel variant blp_solve_* would use for (m, n) (static string). */
 const char *blp_kernel_variant(int32_t m, int32_t n);
 
+/* The same for a batch in the given mode (shared_Ab = 1: support function, one A and b). */
+const char *blp_kernel_variant_mode(int32_t m, int32_t n, int32_t shared_Ab);
+
 /* Number of CUDA kernels this library has launched since load (monotonic). */
 int64_t blp_launch_count(void);
 

@@ -40,7 +40,7 @@ _lib = None
 
 # Every function include/blp.h declares; tests/test_native_abi.py checks the exports.
 EXPORTS = ("blp_solve_batch_device", "blp_solve_batch_host", "blp_solve_batch_gather", "blp_shape_supported",
-           "blp_kernel_variant", "blp_launch_count", "blp_last_error", "blp_abi_version",
+           "blp_kernel_variant", "blp_kernel_variant_mode", "blp_launch_count", "blp_last_error", "blp_abi_version",
            "blp_probe_smem_gbs", "blp_probe_fp64_gflops", "blp_box_solve_device", "blp_box_solve_host",
            "blp_certify_batch_device", "blp_certify_batch_host", "blp_certify_reprice_device",
            "blp_certify_reprice_host")
@@ -69,6 +69,8 @@ def load():
     lib.blp_shape_supported.restype = ctypes.c_int
     lib.blp_kernel_variant.argtypes = [ctypes.c_int32, ctypes.c_int32]
     lib.blp_kernel_variant.restype = ctypes.c_char_p
+    lib.blp_kernel_variant_mode.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+    lib.blp_kernel_variant_mode.restype = ctypes.c_char_p
     lib.blp_launch_count.argtypes = []
     lib.blp_launch_count.restype = ctypes.c_int64
     lib.blp_last_error.argtypes = []
@@ -153,8 +155,8 @@ def make_limits(max_iterations=None, anti_cycling=True, degenerate_pivot_limit=N
                   -1 if degenerate_pivot_limit is None else int(degenerate_pivot_limit), 0)
 
 
-def kernel_variant(m: int, n: int) -> str:
-    return load().blp_kernel_variant(m, n).decode()
+def kernel_variant(m: int, n: int, shared_Ab: bool = False) -> str:
+    return load().blp_kernel_variant_mode(m, n, 1 if shared_Ab else 0).decode()
 
 
 def probe_smem_gbs(device: int = 0) -> float:

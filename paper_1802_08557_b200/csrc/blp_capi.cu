@@ -230,13 +230,14 @@ bool plan_cluster(int m, int n, bool forced, Plan *p) {
 }
 
 // BLP_KERNEL=condensed|warplp|pairlp|regtile|cluster|smem forces a family (testing / tuning).
-bool plan_launch(int m, int n, Plan *p) {
+bool plan_launch(int m, int n, Plan *p, bool shared_Ab = false) {
     const char *force = getenv("BLP_KERNEL");
     const bool any = !force || !*force;
     if ((any || strcmp(force, "condensed") == 0) && plan_condensed(m, n, p)) {
         // the multi-warp condensed form (33..128 rows) takes the lazy kernel's deferrals, as
-        // the dense 33..128-row kernels do (below)
-        p->lazy = p->threads > 32 && any && m > 32 && env_int("BLP_LAZY_SMALL", 1) != 0 &&
+        // the dense 33..128-row kernels do (below) -- except in support mode, where the shared
+        // phase 1 applies and the lazy pass only adds work (C4 2e5: 9.18 -> 7.88 ms without it)
+        p->lazy = !shared_Ab && p->threads > 32 && any && m > 32 && env_int("BLP_LAZY_SMALL", 1) != 0 &&
                   blp_cluster::lazy_enabled(m, n);
         if (p->lazy) {
             static thread_local std::string cname;
@@ -341,7 +342,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     int rc = device_sms(dev, &sms);
     if (rc) return rc;
     Plan P;
-    if (!plan_launch(m, n, &P)) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
+    if (!plan_launch(m, n, &P, shared_Ab != 0)) return fail(BLP_ERR_TOO_LARGE, "LP shape exceeds every kernel variant");
     if (P.cluster) return launch_cluster(A, b, c, count, m, n, shared_Ab, lim, status, objective, x, it1, it2, stream);
     BLP_CUDA_TRY(cudaFuncSetAttribute(P.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
     int occ = 0;
@@ -382,7 +383,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     if (p1) {   // support mode: phase 1 + restore_objective once for the shared A, b
         double *st = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256 + slot_bytes);
         BLP_CUDA_TRY(cudaFuncSetAttribute(P.phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-        P.phase1<<<1, 32, P.smem, stream>>>(B, st);
+        P.phase1<<<1, P.threads, P.smem, stream>>>(B, st);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         BLP_CUDA_TRY(cudaGetLastError());
         B.p1state = st;
@@ -812,6 +813,14 @@ int blp_shape_supported(int32_t m, int32_t n) {
     Plan P;
     if (m < 0 || n < 0) return 0;
     return plan_launch(m, n, &P) ? 1 : 0;
+}
+
+const char *blp_kernel_variant_mode(int32_t m, int32_t n, int32_t shared_Ab) {
+    static thread_local std::string name;
+    Plan P;
+    if (!plan_launch(m, n, &P, shared_Ab != 0)) return "unsupported";
+    name = P.name;
+    return name.c_str();
 }
 
 const char *blp_kernel_variant(int32_t m, int32_t n) {

@@ -222,8 +222,40 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     *defer_list = Bl.defer_list;
     *defer_count = Bl.defer_count;
     if (e == cudaSuccess) {
-        fn<<<(unsigned)grid, threads, smem, stream>>>(Bl);
-        e = cudaGetLastError();
+        // BLP_LAZY_PERSIST (pivots, 0 = off): the first pivots' replay history of every resident
+        // CTA -- one contiguous range in the pivot-major layout -- is marked persisting in L2, so
+        // the validation stream of A passing through L2 does not evict it between the replays
+        // that re-read it (ncu, C5: 8.2 GB of the history/column re-reads missed L2 without).
+        const int kp = B.shared_Ab ? 0 : env_int("BLP_LAZY_PERSIST", 16);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cfg.numAttrs = 0;
+        if (kp > 0) {
+            int maxwin = 0, maxpers = 0;
+            cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            size_t want = (size_t)std::min(kp, blp::kLazyMaxPivots) * (size_t)grid * (size_t)(2 * B.m + B.n) * 8;
+            want = std::min(want, (size_t)std::max(0, std::min(maxwin, maxpers)));
+            if (want > 0) {
+                size_t cur = 0;
+                cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+                attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+                attr[0].val.accessPolicyWindow.base_ptr = Bl.gtab;
+                attr[0].val.accessPolicyWindow.num_bytes = want;
+                attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+                attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+            }
+        }
+        e = cudaLaunchKernelEx(&cfg, fn, Bl);
+        if (e == cudaSuccess) e = cudaGetLastError();
     }
     if (env_int("BLP_VERBOSE", 0))
         fprintf(stderr, "blp lazy: m=%d n=%d grid=%lld x %d (%d per SM, ws=%d rp=%d) smem=%zu scratch=%.1f MB\n", B.m, B.n,

@@ -386,17 +386,177 @@ __device__ __forceinline__ void cm_restore(const CmDims &D, CmState<R> &St, unsi
     }
 }
 
+// build_tableau (tableau.py:139-172): row tid into its thread (slots [R, NS) into the tile),
+// validation fused; slot q starts as structural x_q with reduced cost c_q (0 without c: the
+// shared phase-1 prologue).  Returns "some entry is non-finite" (CTA-wide) and n_art.
+template <int NWR, int R, int S, int ST>
+__device__ __forceinline__ bool cm_build(const CmDims &D, CmState<R> &St, unsigned char *smem, CmXch *X,
+                                         const double *Ag, const double *bg, const double *cg, int &n_art) {
+    using C = CmCfg<NWR, R, S, ST>;
+    double *tile = reinterpret_cast<double *>(smem + C::TILE);
+    const int m = D.m, n = D.n;
+    bool nonfinite = false;
+    const bool live = D.row < m;
+    const double bi = live ? bg[D.row] : 0.0;
+    nonfinite |= !isfinite(bi);
+    const bool neg = live && bi < 0.0;
+    const double sgn = neg ? -1.0 : 1.0;
+    St.rhs = live ? __dmul_rn(bi, sgn) : 0.0;
+    {
+        const double *arow = Ag + (size_t)(live ? D.row : 0) * n;
+#pragma unroll
+        for (int c = 0; c < R; ++c) {
+            double v = 0.0;
+            if (live && c < n) {
+                const double x = arow[c];
+                nonfinite |= !isfinite(x);
+                v = __dmul_rn(x, sgn);
+            }
+            St.a[c] = v;
+        }
+        if (live) {                            // padding rows never touch the tile (ST >= m only)
+#pragma unroll
+            for (int c = 0; c < S; ++c) {
+                double v = 0.0;
+                if (R + c < n) {
+                    const double x = arow[R + c];
+                    nonfinite |= !isfinite(x);
+                    v = __dmul_rn(x, sgn);
+                }
+                tile[(size_t)c * ST + D.row] = v;
+            }
+        }
+    }
+    const unsigned negm = __ballot_sync(kFull, neg);
+    if (D.lane == 0) X->nneg[D.warp] = __popc(negm);
+    if (cg && D.row < n) {
+        St.rc = cg[D.row];
+        nonfinite |= !isfinite(St.rc);
+    } else {
+        St.rc = 0.0;
+    }
+    const bool invalid = __syncthreads_or(nonfinite);
+    int art = __popc(negm & ((1u << D.lane) - 1u));
+    n_art = 0;
+#pragma unroll
+    for (int w = 0; w < NWR; ++w) {
+        art += w < D.warp ? X->nneg[w] : 0;
+        n_art += X->nneg[w];
+    }
+    St.basis = neg ? D.nvc + art : n + D.row;
+    St.ppart = neg ? n + D.row : -1;      // the negated row's slack: column -e_row
+    St.prc = 0.0;
+    St.svar = D.row;                       // slot q: structural x_q
+    St.spart = -1;
+    St.rcp = 0.0;
+    St.obj = 0.0;
+    return invalid;
+}
+
+// Phase 1 (simplex.py:168-178): build_auxiliary, _run_phase, the infeasibility test and
+// restore_objective (c-independent).  Returns the status if the LP ends here, else kOptimal.
+template <int NWR, int R, int S, int ST>
+__device__ __forceinline__ int cm_phase1(const CmDims &D, CmState<R> &St, unsigned char *smem, CmXch *X,
+                                         const Limits &lim, int &it1) {
+    cm_price_out<NWR, R, S, ST, true>(D, St, smem, X, nullptr);
+    const WlpPhase p1 = cm_run_phase<NWR, R, S, ST, true>(D, St, smem, X, lim);
+    it1 = p1.iters;
+    if (p1.state == 2) return kIterationLimit;
+    if (p1.state == 1) return kErrPhase1Unbounded;
+    if (fabs(St.obj) > kPhase1ZeroTol) return kInfeasible;
+    __syncthreads();
+    cm_restore<NWR, R, S, ST>(D, St, smem, X);
+    return kOptimal;
+}
+
+// Shared phase 1 (support mode): the restored tableau of the shared A, b, dumped once by
+// cmulti_phase1_kernel and loaded by every direction (coalesced: field-major, thread-minor;
+// the tile copied as is).  info (4 ints after the state): [0] status, [1] phase-1 iterations,
+// [2] mode (0: b >= 0, build as usual; 1: shared).
+template <int NWR, int R, int S, int ST>
+struct CmP1 {
+    static constexpr int ROWS = 32 * NWR;
+    static constexpr int ND = R + 2;                     // a, rhs, prc
+    static constexpr int NI = 4;                         // basis, ppart, svar, spart
+    static constexpr size_t TILE_OFF = (size_t)ROWS * ND;               // doubles
+    static constexpr size_t INT_OFF = TILE_OFF + (size_t)S * ST;         // doubles
+    static constexpr size_t BYTES = INT_OFF * 8 + (size_t)ROWS * NI * 4 + 16;
+};
+
+template <int NWR, int R, int S, int ST>
+__device__ __forceinline__ void cm_dump(const CmDims &D, const CmState<R> &St, const unsigned char *smem,
+                                        double *st) {
+    using P = CmP1<NWR, R, S, ST>;
+    constexpr int ROWS = P::ROWS;
+    const double *tile = reinterpret_cast<const double *>(smem + CmCfg<NWR, R, S, ST>::TILE);
+    int *si = reinterpret_cast<int *>(st + P::INT_OFF);
+    const int t = D.row;
+#pragma unroll
+    for (int c = 0; c < R; ++c) st[c * ROWS + t] = St.a[c];
+    st[R * ROWS + t] = St.rhs;
+    st[(R + 1) * ROWS + t] = St.prc;
+    for (int i = t; i < S * ST; i += ROWS) st[P::TILE_OFF + i] = tile[i];
+    si[t] = St.basis;
+    si[ROWS + t] = St.ppart;
+    si[2 * ROWS + t] = St.svar;
+    si[3 * ROWS + t] = St.spart;
+}
+
+template <int NWR, int R, int S, int ST>
+__device__ __forceinline__ void cm_load(const CmDims &D, CmState<R> &St, unsigned char *smem, const double *st) {
+    using P = CmP1<NWR, R, S, ST>;
+    constexpr int ROWS = P::ROWS;
+    double *tile = reinterpret_cast<double *>(smem + CmCfg<NWR, R, S, ST>::TILE);
+    const int *si = reinterpret_cast<const int *>(st + P::INT_OFF);
+    const int t = D.row;
+#pragma unroll
+    for (int c = 0; c < R; ++c) St.a[c] = st[c * ROWS + t];
+    St.rhs = st[R * ROWS + t];
+    St.prc = st[(R + 1) * ROWS + t];
+    for (int i = t; i < S * ST; i += ROWS) tile[i] = st[P::TILE_OFF + i];
+    St.basis = si[t];
+    St.ppart = si[ROWS + t];
+    St.svar = si[2 * ROWS + t];
+    St.spart = si[3 * ROWS + t];
+    St.obj = 0.0;
+}
+
+// One CTA: the shared polytope's phase 1 into `st` (support mode only).
+template <int NWR, int R, int S, int ST>
+__global__ void __launch_bounds__(32 * NWR, 1) cmulti_phase1_kernel(Batch B, double *st) {
+    using C = CmCfg<NWR, R, S, ST>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    CmXch *X = reinterpret_cast<CmXch *>(smem + C::XCH);
+    int *info = reinterpret_cast<int *>(reinterpret_cast<char *>(st) + CmP1<NWR, R, S, ST>::BYTES - 16);
+    CmDims D;
+    D.m = B.m; D.n = B.n; D.nvc = B.n + B.m;
+    D.lane = threadIdx.x & 31; D.warp = threadIdx.x >> 5; D.row = threadIdx.x;
+    for (int q = threadIdx.x; q < C::NS; q += C::ROWS) reinterpret_cast<double *>(smem + C::RVEC)[q] = 0.0;
+    __syncthreads();
+    CmState<R> St;
+    int n_art = 0, it1 = 0, status = kOptimal;
+    const bool invalid = cm_build<NWR, R, S, ST>(D, St, smem, X, B.A, B.b, nullptr, n_art);
+    if (invalid) status = kInvalid;
+    else if (n_art > 0) status = cm_phase1<NWR, R, S, ST>(D, St, smem, X, B.lim, it1);
+    __syncthreads();
+    cm_dump<NWR, R, S, ST>(D, St, smem, st);
+    if (threadIdx.x == 0) {
+        info[0] = status;
+        info[1] = it1;
+        info[2] = (invalid || n_art > 0) ? 1 : 0;
+    }
+}
+
 template <int NWR, int R, int S, int ST, int kMinBlocks>
 __global__ void __launch_bounds__(32 * NWR, kMinBlocks)
 cmulti_kernel(Batch B) {
     using C = CmCfg<NWR, R, S, ST>;
     extern __shared__ __align__(16) unsigned char smem[];
     CmXch *X = reinterpret_cast<CmXch *>(smem + C::XCH);
-    double *tile = reinterpret_cast<double *>(smem + C::TILE);
     CmDims D;
     D.m = B.m; D.n = B.n; D.nvc = B.n + B.m;
     D.lane = threadIdx.x & 31; D.warp = threadIdx.x >> 5; D.row = threadIdx.x;
-    const int m = D.m, n = D.n, nvc = D.nvc;
+    const int m = D.m, n = D.n;
     {
         double *rvec = reinterpret_cast<double *>(smem + C::RVEC);
         for (int q = threadIdx.x; q < C::NS; q += C::ROWS) rvec[q] = 0.0;   // unused slots read as 0
@@ -420,83 +580,42 @@ cmulti_kernel(Batch B) {
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;
 
-        // ---- build_tableau (tableau.py:139-172): row tid into its thread; validation fused ----
-        bool nonfinite = false;
-        const bool live = D.row < m;
-        const double bi = live ? bg[D.row] : 0.0;
-        nonfinite |= !isfinite(bi);
-        const bool neg = live && bi < 0.0;
-        const double sgn = neg ? -1.0 : 1.0;
-        St.rhs = live ? __dmul_rn(bi, sgn) : 0.0;
-        {
-            const double *arow = Ag + (size_t)(live ? D.row : 0) * n;
-#pragma unroll
-            for (int c = 0; c < R; ++c) {
-                double v = 0.0;
-                if (live && c < n) {
-                    const double x = arow[c];
-                    nonfinite |= !isfinite(x);
-                    v = __dmul_rn(x, sgn);
-                }
-                St.a[c] = v;
-            }
-            if (live) {                            // padding rows never touch the tile (ST >= m only)
-#pragma unroll
-                for (int c = 0; c < S; ++c) {
-                    double v = 0.0;
-                    if (R + c < n) {
-                        const double x = arow[R + c];
-                        nonfinite |= !isfinite(x);
-                        v = __dmul_rn(x, sgn);
-                    }
-                    tile[(size_t)c * ST + D.row] = v;
-                }
-            }
-        }
-        const unsigned negm = __ballot_sync(kFull, neg);
-        if (D.lane == 0) X->nneg[D.warp] = __popc(negm);
-        if (D.row < n) {
-            St.rc = cg[D.row];
-            nonfinite |= !isfinite(St.rc);
-        } else {
-            St.rc = 0.0;
-        }
-        const bool invalid = __syncthreads_or(nonfinite);
-        int art = __popc(negm & ((1u << D.lane) - 1u)), n_art = 0;
-#pragma unroll
-        for (int w = 0; w < NWR; ++w) {
-            art += w < D.warp ? X->nneg[w] : 0;
-            n_art += X->nneg[w];
-        }
-        St.basis = neg ? nvc + art : n + D.row;
-        St.ppart = neg ? n + D.row : -1;      // the negated row's slack: column -e_row
-        St.prc = 0.0;
-        St.svar = D.row;                       // slot q: structural x_q
-        St.spart = -1;
-        St.rcp = 0.0;
-        St.obj = 0.0;
-
         int8_t status = kOptimal;
         int it1 = 0, it2 = 0;
         bool done = false;
-        if (invalid) {
-            status = kInvalid;
-            done = true;
-        } else if (n_art > 0) {
-            cm_price_out<NWR, R, S, ST, true>(D, St, smem, X, cg);            // build_auxiliary
-            const WlpPhase p1 = cm_run_phase<NWR, R, S, ST, true>(D, St, smem, X, B.lim);
-            it1 = p1.iters;
-            if (p1.state == 2) { status = kIterationLimit; done = true; }
-            else if (p1.state == 1) { status = kErrPhase1Unbounded; done = true; }
-            else if (fabs(St.obj) > kPhase1ZeroTol) { status = kInfeasible; done = true; }
-            else {
-                __syncthreads();
-                cm_restore<NWR, R, S, ST>(D, St, smem, X);
+        // support mode with b < 0: phase 1 was solved once by cmulti_phase1_kernel (its info is
+        // re-read per LP -- an L1 hit -- rather than held in registers across the solve)
+        const int *p1info = B.p1state ? reinterpret_cast<const int *>(reinterpret_cast<const char *>(B.p1state) +
+                                                                      CmP1<NWR, R, S, ST>::BYTES - 16) : nullptr;
+        if (p1info && p1info[2] == 1) {
+            const int p1status = p1info[0], p1iters = p1info[1];
+            const bool nonfinite = D.row < n && !isfinite(cg[D.row]);
+            if (__syncthreads_or(nonfinite) || p1status == kInvalid) {
+                status = kInvalid;
+                done = true;
+            } else if (p1status != kOptimal) {
+                status = (int8_t)p1status;
+                it1 = p1iters;
+                done = true;
+            } else {
+                it1 = p1iters;
+                cm_load<NWR, R, S, ST>(D, St, smem, B.p1state);
                 cm_price_out<NWR, R, S, ST, false>(D, St, smem, X, cg);
             }
         } else {
-            cm_candidates<NWR, R, false>(D, St, X, false, -1, 0.0);
-            __syncthreads();
+            int n_art = 0;
+            const bool invalid = cm_build<NWR, R, S, ST>(D, St, smem, X, Ag, bg, cg, n_art);
+            if (invalid) {
+                status = kInvalid;
+                done = true;
+            } else if (n_art > 0) {
+                const int st = cm_phase1<NWR, R, S, ST>(D, St, smem, X, B.lim, it1);
+                if (st != kOptimal) { status = (int8_t)st; done = true; }
+                else cm_price_out<NWR, R, S, ST, false>(D, St, smem, X, cg);
+            } else {
+                cm_candidates<NWR, R, false>(D, St, X, false, -1, 0.0);
+                __syncthreads();
+            }
         }
         if (!done) {
             const WlpPhase p2 = cm_run_phase<NWR, R, S, ST, false>(D, St, smem, X, B.lim);

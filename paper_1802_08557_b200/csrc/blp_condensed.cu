@@ -40,7 +40,8 @@ const Row kInstances[] = {
 struct MRow { int nwr, ns, r; Instance inst; };
 #define CM_INST(NWR, R, S, ST, MB)                                                                     \
     {NWR, R + S, R, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
-                  blp::CmCfg<NWR, R, S, ST>::BYTES, nullptr, 0, 32 * NWR}}
+                  blp::CmCfg<NWR, R, S, ST>::BYTES, blp::cmulti_phase1_kernel<NWR, R, S, ST>,                \
+                  blp::CmP1<NWR, R, S, ST>::BYTES, 32 * NWR}}
 // First fit in this order.  C3 (100 x 100, c3 count 2e4, device-resident): r48_s56 at 3 LPs
 // per SM 74.8 ms; r88_s16 (2 per SM) 88.0; r80_s24 89.5; r64_s40 94.7; r96_s32 107.7.
 const MRow kMulti[] = {
@@ -67,9 +68,10 @@ int rows_per_lane(int m) { return m <= 32 ? 1 : (m <= 64 ? 2 : (m <= 128 ? 4 : 0
 
 bool select(int m, int n, Instance *out) {
     if (m < 1 || n < 1) return false;
-    // BLP_CMULTI: 0 never, 1 (default) for 65..128 rows and where the one-warp form has no
-    // instance, 2 for every 33..128-row shape
-    const int cm = env_int("BLP_CMULTI", 1);
+    // BLP_CMULTI: 0 never, 1 for 65..128 rows and where the one-warp form has no instance,
+    // 2 (default) for every 33..128-row shape (C4 64 x 32, 2e5 directions: cm2_r32_s0 7.88 ms,
+    // the one-warp ctab_r2_s32 8.71)
+    const int cm = env_int("BLP_CMULTI", 2);
     if (m > 32 && m <= 128 && cm != 0) {
         const int nwr = m <= 64 ? 2 : 4;
         const bool one_warp_fits = (m <= 64 && n <= 32) || (m > 64 && n <= 16);

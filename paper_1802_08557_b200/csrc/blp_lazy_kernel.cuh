@@ -212,8 +212,12 @@ lazy_kernel(Batch B) {
     unsigned gseq = 0;                                       // ring chunks consumed (scanner warps)
     auto pbar = [&]() { if (WS) lazy_bar(1, PT); else __syncthreads(); };
     // history: F[t] (m doubles), R[t] (nv doubles), t = 0 .. kLazyMaxPivots-1 (pivot t+1)
-    double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)B.gtab_stride;
-    double *Rh = Fh + (size_t)kLazyMaxPivots * m;
+    // history layout: pivot-major across the CTAs -- row t of CTA b (f^t: m doubles, then
+    // r^t: nv) at ((t * G + b) * (m + nv)) -- so the first pivots' history of every resident
+    // CTA is one contiguous range (the launch marks it persisting in L2; launch_lazy)
+    const size_t HS = (size_t)gridDim.x * (size_t)(m + nv);     // pivot t -> t+1, same CTA
+    double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)(m + nv);
+    double *Rh = Fh + m;
     double *Fs = nullptr;
     int KF = 0;
     if constexpr (FS) {
@@ -225,7 +229,7 @@ lazy_kernel(Batch B) {
     }
     auto Fget = [&](int t, int i) -> double {
         if constexpr (FS) { if (t < KF) return Fs[(size_t)t * m + i]; }
-        return lazy_h(Fh + (size_t)t * m + i);
+        return lazy_h(Fh + (size_t)t * HS + i);
     };
     const int max_iter = B.lim.max_iterations > 0 ? B.lim.max_iterations : 50 * (m + n);
     const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
@@ -377,7 +381,7 @@ lazy_kernel(Batch B) {
                 unsigned long long lk = kKeyEmptyMin;
                 int li = kNone;
                 if constexpr (RP == 1) {
-                    for (int t = lane; t < k; t += 32) hw[t] = lazy_h(Rh + (size_t)t * nv + e);   // r^t_e
+                    for (int t = lane; t < k; t += 32) hw[t] = lazy_h(Rh + (size_t)t * HS + e);   // r^t_e
                     __syncwarp();
                 }
                 for (int i = tid; i < m; i += PT) {
@@ -385,15 +389,15 @@ lazy_kernel(Batch B) {
                     double a;
                     if constexpr (RP == 1) {
                         a = t0 ? hw[t0 - 1] : lazy_a0(Ag, n, i, e);
-                        a = lazy_replay(a, Fh + i, m, hw, t0, k);
+                        a = lazy_replay(a, Fh + i, (int)HS, hw, t0, k);
                     } else {
-                        a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * nv + e) : lazy_a0(Ag, n, i, e);
+                        a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * HS + e) : lazy_a0(Ag, n, i, e);
                         for (int t = t0; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), lazy_h(Rh + (size_t)t * nv + e)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), lazy_h(Rh + (size_t)t * HS + e)));
                     }
                     fcur[i] = a;
                     if (FS && k < KF) Fs[(size_t)k * m + i] = a;
-                    else Fh[(size_t)k * m + i] = a;
+                    else Fh[(size_t)k * HS + i] = a;
                     const unsigned long long key = key_min(ratio_entry(rhs[i], a));
                     if (key < lk) { lk = key; li = i; }     // rows ascend per thread
                 }
@@ -426,19 +430,19 @@ lazy_kernel(Batch B) {
                 // pivot row by replay, divided by pe; objective row; next candidates
                 unsigned long long ck = kKeyEmptyMax;
                 int ci = kNone, cb = kNone;
-                double *Rk = Rh + (size_t)k * nv;
+                double *Rk = Rh + (size_t)k * HS;
                 if constexpr (RP == 1) {
                     __syncwarp();
                     for (int t = t0l + lane; t < k; t += 32) hw[t] = Fget(t, l);   // f^t_l
                     __syncwarp();
                 }
                 for (int j = tid; j < nv; j += PT) {
-                    double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * nv + j) : lazy_a0(Ag, n, l, j);
+                    double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * HS + j) : lazy_a0(Ag, n, l, j);
                     if constexpr (RP == 1) {
-                        a = lazy_replay(a, Rh + j, nv, hw, t0l, k);
+                        a = lazy_replay(a, Rh + j, (int)HS, hw, t0l, k);
                     } else {
                         for (int t = t0l; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), lazy_h(Rh + (size_t)t * nv + j)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), lazy_h(Rh + (size_t)t * HS + j)));
                     }
                     const double r = div_entry(a, pe);
                     Rk[j] = r;

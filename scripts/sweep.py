@@ -22,8 +22,23 @@ p.add_argument("--count", type=int, default=None)
 p.add_argument("--steps", type=int, default=5)
 p.add_argument("--env", nargs="*", default=[""])
 p.add_argument("--max-iter", type=int, default=None, help="SolverLimits.max_iterations (per phase): isolates build cost")
+p.add_argument("--shape", default=None, help="recipe:m:n instead of a config (afiro | degenerate | random)")
 a = p.parse_args()
-A, b, c, shared, spec = bench.workload(a.config, a.count, 0)
+if a.shape:
+    from paper_1802_08557_b200 import workloads
+    kind, sm, sn = a.shape.split(":")
+    sm, sn, cnt0 = int(sm), int(sn), a.count or 100_000
+    if kind == "afiro":
+        A, b, c = workloads.afiro_arrays(cnt0, seed=9, m=sm, n=sn)
+    elif kind == "degenerate":
+        A, b, c = workloads.degenerate_arrays(cnt0, seed=9, m=sm, n=sn)
+    else:
+        A, b, c = workloads.random_arrays(max(sm, sn), cnt0, 9)
+        A, b, c = A[:, :sm, :sn].copy(), b[:, :sm].copy(), c[:, :sn].copy()
+    shared = False
+    a.config = a.shape
+else:
+    A, b, c, shared, spec = bench.workload(a.config, a.count, 0)
 dev = torch.device("cuda:0")
 tA, tb, tc = (torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (A, b, c))
 cnt, n = c.shape
@@ -58,7 +73,7 @@ for setting in a.env:
         same = all(np.array_equal(ref[k], res[k]) for k in ("status", "it1", "it2", "x"))
     ms = statistics.median(ts)
     piv = int((res["it1"].astype(np.int64) + res["it2"]).sum())
-    print(json.dumps({"config": a.config, "env": setting, "variant": _native.kernel_variant(m, n), "ms": ms,
+    print(json.dumps({"config": a.config, "env": setting, "variant": _native.kernel_variant(m, n, shared), "ms": ms,
                       "lps_per_s": cnt / ms * 1e3, "pivots_per_s": piv / ms * 1e3,
                       "gbs_alg": piv * bench.bytes_per_pivot(m, n) / ms / 1e6, "same_as_first": same}), flush=True)
     os.environ.clear()

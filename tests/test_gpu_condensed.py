@@ -118,7 +118,7 @@ def test_condensed_reference_records(condensed):
     checked = 0
     for fixture in ("known.json", "ragged.json"):
         for rec in json_records(fixture):
-            if not _native.kernel_variant(rec["m"], rec["n"]).startswith("ctab"):
+            if not _native.kernel_variant(rec["m"], rec["n"]).startswith(("ctab", "cm")):
                 continue
             res = batch_solve_arrays(rec["A"][None], rec["b"][None], rec["c"][None], SolverLimits(**rec["limits"]))
             o = rec["outcome"]
@@ -134,7 +134,7 @@ def test_condensed_packed_goldens(stem, condensed):
     from paper_1802_08557_b200 import _native, batch_solve_arrays, support_batch
     fx = packed_fixture(stem)
     m, n = fx["b"].shape[-1], fx["c"].shape[1]
-    if not _native.kernel_variant(m, n).startswith("ctab"):
+    if not _native.kernel_variant(m, n, fx["shared"]).startswith(("ctab", "cm")):
         pytest.skip(f"{m}x{n} outside the condensed family")
     res = support_batch(fx["A"], fx["b"], fx["c"]) if fx["shared"] else batch_solve_arrays(fx["A"], fx["b"], fx["c"])
     compare(_d(res), fx, stem)

@@ -38,21 +38,26 @@ def test_c4b_directions_match_oracle():
     A, b = workloads.support_polytope_two_phase()
     C = workloads.support_directions(20_000)
     assert (b < 0).sum() == 16
-    assert _native.kernel_variant(64, 32).startswith("ctab")
+    assert _native.kernel_variant(64, 32, True).startswith(("ctab", "cm"))
     got = _solve(A, b, C)
     want = oracle.solve_batch(A, b, C, shared_Ab=True, threads=oracle.host_cores())
     compare(_d(got), want, "c4b 20k directions")
     assert (got["it1"] == want["it1"][0]).all() and want["it1"][0] > 0
 
 
-@pytest.mark.parametrize("m,n", [(20, 12), (28, 32), (40, 16), (64, 8), (100, 12)])
-def test_shared_phase1_every_condensed_shape(m, n, monkeypatch):
-    """Every one-warp condensed instance family (rows per lane 1/2/4) with a mixed-sign
-    shared b: afiro-recipe polytopes, feasible and infeasible, random directions."""
+@pytest.mark.parametrize("cm", ["0", "2"])
+@pytest.mark.parametrize("m,n", [(20, 12), (28, 32), (40, 16), (64, 8), (100, 12), (64, 32), (100, 100), (120, 128)])
+def test_shared_phase1_every_condensed_shape(m, n, cm, monkeypatch):
+    """Every condensed instance family -- one warp (rows per lane 1/2/4; BLP_CMULTI=0) and
+    multi-warp (cmulti, registers + tile; BLP_CMULTI=2) -- with a mixed-sign shared b:
+    afiro-recipe polytopes, feasible and infeasible, random directions."""
     from oracle import oracle
     from paper_1802_08557_b200 import _native, workloads
-    monkeypatch.setenv("BLP_CMULTI", "0")
-    assert _native.kernel_variant(m, n).startswith("ctab")
+    monkeypatch.setenv("BLP_CMULTI", cm)
+    variant = _native.kernel_variant(m, n, True)
+    if not variant.startswith(("ctab", "cm")):
+        pytest.skip(f"{m}x{n}: no one-warp instance")
+    assert variant.startswith("cm" if cm == "2" and m > 32 else "ctab"), variant
     for seed in range(4):
         A, b, _ = workloads.afiro_arrays(1, seed=100 + seed, m=m, n=n, infeasible_frac=0.5)
         C = np.random.default_rng(seed).integers(-20, 51, size=(300, n)).astype(np.float64)
