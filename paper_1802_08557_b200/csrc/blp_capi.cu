@@ -306,6 +306,8 @@ void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c
     B.defer_list = nullptr;
     B.defer_count = nullptr;
     B.p1state = nullptr;
+    B.vq = nullptr;
+    B.vflag = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -328,7 +330,9 @@ int launch_cluster(const double *A, const double *b, const double *c, long long 
     const cudaError_t e = blp_cluster::lazy_enabled(m, n) ? blp_cluster::launch_lazy_then_cluster(B, stream)
                                                            : blp_cluster::launch(B, stream, &K, &clusters);
     if (e != cudaSuccess) return fail(BLP_ERR_CUDA, std::string("cluster launch: ") + cudaGetErrorString(e));
-    g_launches.fetch_add(blp_cluster::lazy_enabled(m, n) ? (shared_Ab ? 4 : 2) : 1, std::memory_order_relaxed);   // lazy, cluster (+ validate, finalize)
+    // lazy, cluster (+ validate and/or finalize)
+    g_launches.fetch_add(blp_cluster::lazy_enabled(m, n) ? 2 + blp_cluster::finish_lazy_launches(B) : 1,
+                         std::memory_order_relaxed);
     return BLP_OK;
 }
 
@@ -375,6 +379,8 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.defer_list = defer_list;
     B.defer_count = defer_count;
     B.p1state = nullptr;
+    B.vq = nullptr;
+    B.vflag = nullptr;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -392,7 +398,10 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     g_launches.fetch_add(1, std::memory_order_relaxed);
     BLP_CUDA_TRY(cudaGetLastError());
     BLP_CUDA_TRY(cudaFreeAsync(ws, stream));
-    if (P.lazy) BLP_CUDA_TRY(blp_cluster::finish_lazy(B, stream, lazy_ws));
+    if (P.lazy) {
+        BLP_CUDA_TRY(blp_cluster::finish_lazy(B, stream, lazy_ws));
+        g_launches.fetch_add(blp_cluster::finish_lazy_launches(B), std::memory_order_relaxed);
+    }
     return BLP_OK;
 }
 

@@ -145,6 +145,25 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
     return e != cudaSuccess ? e : ef;
 }
 
+static int lazy_ws_mode(const blp::Batch &B, int nt) {
+    return (nt == 512 && !B.shared_Ab && env_int("BLP_LAZY_WS", 0)) ? 1 : 0;
+}
+
+static int lazy_nt(const blp::Batch &B) {
+    const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 512));
+    return env_int("BLP_LAZY_NT", dflt);
+}
+
+// BLP_LAZY_SPLIT=1 (opt-in, parity-tested): validation of A as its own work queue
+// (independent LPs, non-WS form; blp_lazy_kernel.cuh), made BLP_STATUS_INVALID by
+// lazy_finalize_kernel afterwards.  Measured slower: C5 1e4 5.54 ms vs 5.12 inline, random
+// 100 x 100 2e4 0.91 vs 0.86 -- a solve is a chain of ~5 us pivots, so the CTAs that solve
+// while the others stream are too few; inline, every CTA overlaps its neighbour's stream.
+static bool lazy_split(const blp::Batch &B) {
+    return !B.shared_Ab && (long long)B.m * B.n > 0 && !lazy_ws_mode(B, lazy_nt(B)) &&
+           env_int("BLP_LAZY_SPLIT", 0) != 0;
+}
+
 cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_list, int **defer_count, void **ws_out) {
     using LazyFn = void (*)(blp::Batch);
     // BLP_LAZY_NT: threads per CTA (resident CTAs per SM follow from the register budget).
@@ -152,13 +171,12 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     // 256 -> 1.21, 64 -> 0.99; 64 x 64: 64 -> 0.42, 128 -> 0.51, 32 -> 0.48; support mode (no
     // per-LP scan of A) C4 1e6: 32 -> 65.4 ms, 64 -> 70.7, 128 -> 81.5 (dense pairlp: 77.3)
     // (after the unrolled validation scan, C5: 512 -> 5.43 ms, 256 -> 5.75)
-    const int dflt = B.shared_Ab ? (B.m <= 64 ? 32 : 64) : (B.m <= 64 ? 64 : (B.m <= 128 ? 128 : 512));
-    const int nt = env_int("BLP_LAZY_NT", dflt);
+    const int nt = lazy_nt(B);
     // BLP_LAZY_WS=1: the warp-specialised bulk-copy validation stream (measured slower on
     // C5: 6.7 vs 6.0 ms -- the solve, not the stream, bounds an LP); the staged replay
     // (RP=1) only for the shared polytope (C4 1e6: 60.2 vs 65.0 ms; C5 5.87 vs 5.43,
     // random 100 x 100 0.98 vs 0.83)
-    const int ws_mode = (nt == 512 && !B.shared_Ab && env_int("BLP_LAZY_WS", 0)) ? 1 : 0;
+    const int ws_mode = lazy_ws_mode(B, nt);
     const int rp = env_int("BLP_LAZY_RP", B.shared_Ab ? 1 : 0) ? 1 : 0;
     LazyFn fn;
     if (ws_mode) fn = rp ? (LazyFn)blp::lazy_kernel<512, 2, 1, 1> : (LazyFn)blp::lazy_kernel<512, 2, 1, 0>;
@@ -219,6 +237,10 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     Bl.defer_list = reinterpret_cast<int *>(ws + 256);
     Bl.gtab = reinterpret_cast<double *>(ws + 256 + list_bytes + flag_bytes);
     Bl.gtab_stride = stride;
+    const bool split = lazy_split(B);
+    Bl.vq = split ? reinterpret_cast<int *>(ws + 128) : nullptr;
+    Bl.vflag = split ? flags : nullptr;
+    if (split && e == cudaSuccess) e = cudaMemsetAsync(flags, 0, flag_bytes, stream);
     *defer_list = Bl.defer_list;
     *defer_count = Bl.defer_count;
     if (e == cudaSuccess) {
@@ -271,16 +293,24 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
 // Support mode only: after the dense kernel, mark every LP invalid if the shared
 // polytope holds a non-finite entry (the lazy kernel does not scan A then).
 static cudaError_t launch_lazy_finalize(const blp::Batch &B, cudaStream_t stream, void *ws) {
-    if (!B.shared_Ab || (long long)B.m * B.n == 0) return cudaSuccess;
+    const bool split = lazy_split(B);
+    if (!split && (!B.shared_Ab || (long long)B.m * B.n == 0)) return cudaSuccess;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t list_bytes = ((size_t)B.count * sizeof(int) + 255) / 256 * 256;
     unsigned char *flags = reinterpret_cast<unsigned char *>(static_cast<char *>(ws) + 256 + list_bytes);
-    blp::lazy_validate_kernel<<<1, 256, 0, stream>>>(B.A, B.count, (long long)B.m * B.n, 1, flags);
+    // support mode: the shared polytope is validated here; split mode: the lazy kernel's
+    // validation queue already set the flags
+    if (!split) blp::lazy_validate_kernel<<<1, 256, 0, stream>>>(B.A, B.count, (long long)B.m * B.n, 1, flags);
     blp::lazy_finalize_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>((B.count + 255) / 256, 4LL * sms)),
                                 256, 0, stream>>>(flags, B);
     return cudaGetLastError();
+}
+
+int finish_lazy_launches(const blp::Batch &B) {
+    if (lazy_split(B)) return 1;
+    return (B.shared_Ab && (long long)B.m * B.n > 0) ? 2 : 0;
 }
 
 cudaError_t finish_lazy(const blp::Batch &B, cudaStream_t stream, void *ws) {

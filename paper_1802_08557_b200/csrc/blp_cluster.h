@@ -39,4 +39,8 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
 // the workspace is released (stream-ordered).
 cudaError_t finish_lazy(const blp::Batch &B, cudaStream_t stream, void *ws);
 
+// Kernels finish_lazy launches for this batch (support-mode validate + finalize, or the
+// split mode's finalize), for blp_launch_count.
+int finish_lazy_launches(const blp::Batch &B);
+
 }  // namespace blp_cluster

@@ -68,6 +68,9 @@ struct Batch {
     // Shared phase 1 (support mode, condensed kernels): the restored post-phase-1 tableau
     // and its status, written once per batch by condensed_phase1_kernel; null otherwise.
     const double *p1state;
+    // Lazy kernel split mode: validation-chunk queue head and per-LP "non-finite A" flags
+    int *vq;
+    unsigned char *vflag;
 };
 
 // Number of LPs a kernel launch processes, and the batch index of its k-th.

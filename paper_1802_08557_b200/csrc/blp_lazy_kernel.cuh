@@ -235,11 +235,60 @@ lazy_kernel(Batch B) {
     const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
     const unsigned long long kSent = key_max(kSentinel), kDeg = key_max(kDegenerateTol), kTolK = key_max(kTol);
 
+    // Split mode (B.vq set; independent LPs, non-WS form): the validation of A runs as its own
+    // work queue instead of inline before each solve.  The first half of the CTAs take
+    // validation chunks (one LP's A each) first, the second half LPs to solve first; a CTA whose
+    // queue is empty takes from the other one, so the HBM stream of A (the kernel's floor)
+    // overlaps the latency-bound solves across CTAs.  A flagged LP is made BLP_STATUS_INVALID
+    // by lazy_finalize_kernel after the launch sequence.
+    const bool split = !WS && !B.shared_Ab && B.vq != nullptr;
+    const bool validator_first = split && blockIdx.x < gridDim.x / 2;
     for (;;) {
-        if (tid == 0) *s_lp = atomicAdd(B.next_lp, 1);
+        if (tid == 0) {
+            long long got = B.count;
+            int kind = 0;
+            if (!split) {
+                got = atomicAdd(B.next_lp, 1);
+            } else {
+                for (int attempt = 0; attempt < 2 && got >= B.count; ++attempt) {
+                    kind = (attempt == 0) == validator_first ? 1 : 0;
+                    if (kind == 1 ? *((volatile int *)B.vq) < B.count : *((volatile int *)B.next_lp) < B.count)
+                        got = atomicAdd(kind == 1 ? B.vq : B.next_lp, 1);
+                }
+            }
+            *s_lp = got;
+            s_res[3] = kind;
+        }
         __syncthreads();
         const long long lp = *s_lp;
         if (lp >= B.count) break;
+        if (split && s_res[3] == 1) {
+            // ---- validation chunk (model.py:263-301): every entry of LP lp's A, streamed once ----
+            const double *Av = B.A + (size_t)lp * m * n;
+            const size_t total = (size_t)m * n;
+            const size_t head = ((reinterpret_cast<size_t>(Av) & 15) != 0) ? 1 : 0;
+            bool bad = false;
+            if (tid == 0 && head && total) bad |= !isfinite(Av[0]);
+            const double2 *A2 = reinterpret_cast<const double2 *>(Av + head);
+            const size_t n2 = (total - head) / 2;
+            size_t q = tid;
+            constexpr int U = NT >= 512 ? 6 : LAZY_SCAN_U;
+            for (; q + (U - 1) * NT < n2; q += U * NT) {
+                double2 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = lazy_scan_load(A2 + q + u * NT);
+#pragma unroll
+                for (int u = 0; u < U; ++u) bad |= !(isfinite(v[u].x) && isfinite(v[u].y));
+            }
+            for (; q < n2; q += NT) {
+                const double2 v = __ldcs(A2 + q);
+                bad |= !(isfinite(v.x) && isfinite(v.y));
+            }
+            if (tid == 0 && ((total - head) & 1)) bad |= !isfinite(Av[total - 1]);
+            if (bad) B.vflag[lp] = 1;
+            __syncthreads();   // s_lp / s_res are rewritten by the next claim
+            continue;
+        }
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;
@@ -262,7 +311,7 @@ lazy_kernel(Batch B) {
         // ---- validate (model.py:263-301): every entry of A, streamed once; b above, c below ----
         // (Measured, not kept: the stream after the solve, so the solve's reads of A are still in
         // L2 when it passes them -- 1.1 GB less DRAM per C5 launch but 5.18 -> 5.36 ms.)
-        if (!WS && !B.shared_Ab) {
+        if (!WS && !B.shared_Ab && !split) {
             const size_t total = (size_t)m * n;
             const size_t head = ((reinterpret_cast<size_t>(Ag) & 15) != 0) ? 1 : 0;   // 16-byte align the body
             if (tid == 0 && head && total) nonfinite |= !isfinite(Ag[0]);
