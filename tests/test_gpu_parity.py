@@ -341,6 +341,17 @@ def test_lazy_tableau_matches_oracle(m, n, monkeypatch):
         compare(_native_dict(got), want, f"lazy {m}x{n} max_iterations={mi}")
 
 
+def test_lazy_split_mode_matches_oracle(monkeypatch):
+    """BLP_LAZY_SPLIT=1 (validation as its own queue) on the single-phase mix, 150 x 150 and
+    100 x 100 (lazy ahead of cmulti): equal to the oracle."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import batch_solve_arrays
+    monkeypatch.setenv("BLP_LAZY_SPLIT", "1")
+    for m, n in ((150, 150), (100, 100)):
+        A, b, c = _single_phase_mix(m, n, seed=m + 3)
+        compare(_native_dict(batch_solve_arrays(A, b, c)), oracle.solve_batch(A, b, c), f"lazy split {m}x{n}")
+
+
 def test_lazy_disabled_matches_lazy(monkeypatch):
     """BLP_LAZY=0 (dense cluster kernel for everything) gives the same bits."""
     from paper_1802_08557_b200 import batch_solve_arrays
@@ -389,11 +400,14 @@ def test_lazy_support_staged_replay_matches_plain(monkeypatch):
         assert np.array_equal(r1[k], r2[k], equal_nan=True), k
 
 
-def test_lazy_path_flags_non_finite_entries():
-    """A non-finite entry anywhere in A (found by the concurrent validation pass), b or c
-    of a lazy-path batch: that LP comes back BLP_STATUS_INVALID, the others solved."""
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_lazy_path_flags_non_finite_entries(split, monkeypatch):
+    """A non-finite entry anywhere in A (found by the concurrent validation pass -- inline, or
+    the split mode's validation queue + finalize), b or c of a lazy-path batch: that LP comes
+    back BLP_STATUS_INVALID, the others solved."""
     from oracle import oracle
     from paper_1802_08557_b200 import _native, workloads
+    monkeypatch.setenv("BLP_LAZY_SPLIT", split)
     A, b, c = workloads.random_arrays(150, 12, seed=9)
     A[3, 149, 148] = np.nan
     A[5, 0, 0] = np.inf
