@@ -166,9 +166,12 @@ def ncu_traffic(cfg: str, variant: str, count: int):
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
-    for rec in json.loads(p.read_text()):
-        if rec.get("config") == cfg and rec.get("variant") == variant and rec.get("lps_per_launch") == count:
+    recs = [r for r in json.loads(p.read_text()) if r.get("config") == cfg and r.get("variant") == variant]
+    for rec in recs:
+        if rec.get("lps_per_launch") == count:
             return rec.get("dram_bytes_per_launch")
+    for rec in recs:   # a capture on a sub-batch of the same workload: per-LP traffic x LPs
+        return rec["dram_bytes_per_launch"] / rec["lps_per_launch"] * count
     return None
 
 
