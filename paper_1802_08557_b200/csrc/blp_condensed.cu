@@ -44,8 +44,10 @@ struct MRow { int nwr, ns, r; Instance inst; };
                   blp::CmP1<NWR, R, S, ST>::BYTES, 32 * NWR}}
 // First fit in this order.  C3 (100 x 100, c3 count 2e4, device-resident): r48_s56 at 3 LPs
 // per SM 74.8 ms; r88_s16 (2 per SM) 88.0; r80_s24 89.5; r64_s40 94.7; r96_s32 107.7.
+// C4 (64 x 32 support, 1e6): r16_s16 at 10 LPs per SM 38.4 ms; r32_s0 (8 per SM) 39.4;
+// r24_s8 39.9; afiro 64 x 32 (1e5): 16.1 / 18.3 / 18.3 ms.
 const MRow kMulti[] = {
-    CM_INST(2, 32, 0, 65, 8),
+    CM_INST(2, 16, 16, 65, 10),
     CM_INST(2, 64, 0, 65, 4),
     CM_INST(4, 32, 0, 129, 4),
     CM_INST(4, 48, 16, 129, 3),
@@ -55,6 +57,8 @@ const MRow kMulti[] = {
     CM_INST(4, 88, 16, 129, 2),
     CM_INST(4, 80, 24, 129, 2),
     CM_INST(4, 64, 40, 129, 2),
+    CM_INST(2, 32, 0, 65, 8),
+    CM_INST(2, 24, 8, 65, 10),
 };
 #undef CM_INST
 

@@ -38,7 +38,7 @@ def test_host_only_entry_points():
     assert lib.blp_launch_count() >= 0
 
 
-@pytest.mark.parametrize("m,n,family", [(5, 5, "ctab_r1_s8"), (28, 32, "ctab_r1_s32"), (64, 32, "lazy+cm2_r32_s0"),
+@pytest.mark.parametrize("m,n,family", [(5, 5, "ctab_r1_s8"), (28, 32, "ctab_r1_s32"), (64, 32, "lazy+cm2_r16_s16"),
                                         (100, 100, "lazy+cm4_r48_s56"), (50, 50, "lazy+cm2_r64_s0"), (100, 150, "lazy+smem"),
                                         (90, 140, "lazy+smem"), (64, 40, "lazy+cm2_r64_s0"),
                                         (500, 500, "lazy+cluster"),
@@ -50,7 +50,7 @@ def test_kernel_variant_selection(m, n, family):
 def test_kernel_variant_support_mode():
     """Support mode (one A, b): the condensed kernels run without the lazy pass ahead of
     them (their shared phase 1 applies instead)."""
-    assert _native.kernel_variant(64, 32, True) == "cm2_r32_s0"
+    assert _native.kernel_variant(64, 32, True) == "cm2_r16_s16"
     assert _native.kernel_variant(28, 32, True) == "ctab_r1_s32"
     assert _native.kernel_variant(100, 100, True) == "cm4_r48_s56"
 
