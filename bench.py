@@ -160,19 +160,23 @@ def measured_hbm_gbs() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg: str, variant: str, count: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel, from the committed
-    `ncu --set full` capture summary (profiles/traffic.json, scripts/ncu_summary.py), or None."""
+def ncu_record(cfg: str, variant: str):
+    """The committed `ncu --set full` capture summary of this config's kernel
+    (profiles/traffic.json, written by scripts/ncu_summary.py), or None."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
     recs = [r for r in json.loads(p.read_text()) if r.get("config") == cfg and r.get("variant") == variant]
-    for rec in recs:
-        if rec.get("lps_per_launch") == count:
-            return rec.get("dram_bytes_per_launch")
-    for rec in recs:   # a capture on a sub-batch of the same workload: per-LP traffic x LPs
-        return rec["dram_bytes_per_launch"] / rec["lps_per_launch"] * count
-    return None
+    return recs[-1] if recs else None
+
+
+def ncu_traffic(cfg: str, variant: str, count: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel from the committed
+    capture (per-LP traffic x LPs when the capture used a sub-batch of the workload), or None."""
+    rec = ncu_record(cfg, variant)
+    if rec is None:
+        return None
+    return rec["dram_bytes_per_launch"] / rec["lps_per_launch"] * count
 
 
 def cpu_baseline(A, b, c, shared, target_s: float = 10.0) -> tuple[dict, dict]:
@@ -375,6 +379,11 @@ def main():
                              smem_peak=_native.probe_smem_gbs(local_dev),
                              fp64_peak=_native.probe_fp64_gflops(local_dev) / 1e3,
                              traffic=ncu_traffic(args.config, variant, count))
+    rec = ncu_record(args.config, variant)
+    if rec is not None:
+        # what the committed capture says binds the kernel (pipe utilisations, 0..1)
+        roofline["ncu"] = {k: rec.get(k) for k in ("issue_active", "fp64_pipe", "smem_pipe")} | \
+                          {"source": rec.get("source")}
 
     # ---- e2e through the public API from pinned host buffers, on this rank's GPU ----
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731

@@ -45,7 +45,11 @@ for vals in rows[2:]:
     rb *= scale.get(u.get("dram__bytes_read.sum", "byte"), 1)
     wb *= scale.get(u.get("dram__bytes_write.sum", "byte"), 1)
     lines.append(f"  dram bytes per launch = {rb + wb:.0f}")
-    traffic.append(dict(kernel=name, dram_bytes_per_launch=rb + wb))
+    pct = lambda k: round(float(d[k].replace(",", "")) / 100, 4) if d.get(k) else None  # noqa: E731
+    traffic.append(dict(kernel=name, dram_bytes_per_launch=rb + wb,
+                        issue_active=pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                        fp64_pipe=pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                        smem_pipe=pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")))
 Path(a.out).write_text("\n".join(lines) + "\n")
 print("\n".join(lines))
 variant = None
@@ -67,5 +71,6 @@ for t in traffic:
     recs = [r for r in recs if not (r["config"] == a.config and r["lps_per_launch"] == a.lps
                                     and (r["kernel"] == t["kernel"] or r["variant"] == t["variant_family"]))]
     recs.append(dict(config=a.config, lps_per_launch=a.lps, kernel=t["kernel"], variant=t["variant_family"],
-                     dram_bytes_per_launch=t["dram_bytes_per_launch"], source=a.out))
+                     dram_bytes_per_launch=t["dram_bytes_per_launch"], issue_active=t["issue_active"],
+                     fp64_pipe=t["fp64_pipe"], smem_pipe=t["smem_pipe"], source=a.out))
 tj.write_text(json.dumps(recs, indent=1) + "\n")
