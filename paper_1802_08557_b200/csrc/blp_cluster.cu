@@ -265,7 +265,13 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
             if (want > 0) {
                 size_t cur = 0;
                 cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-                if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+                if (cur < want) {
+                    const cudaError_t le = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+                    if (le != cudaSuccess) cudaGetLastError();   // not fatal: the window is a hint
+                    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+                }
+                if (env_int("BLP_VERBOSE", 0))
+                    fprintf(stderr, "blp lazy: persisting window %zu B (limit %zu B, max %d)\n", want, cur, maxpers);
                 attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
                 attr[0].val.accessPolicyWindow.base_ptr = Bl.gtab;
                 attr[0].val.accessPolicyWindow.num_bytes = want;
