@@ -877,11 +877,11 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
         return solve_host_staged(src, count, m, n, shared_Ab, limits, status, objective, x, iters1, iters2,
                                  device, ss);
     }
-    // Sub-batches: at least 8192 LPs each, at most 8 of them.
-    // Sub-batches: BLP_HOST_CHUNKS of them (default 32), at least 2048 LPs each
-    // (measured on C2: 4 -> 17.0 ms, 8 -> 15.5, 16 -> 15.2, 32 -> 14.9, 64 -> 15.2 per 1e5,
-    // against a 13.8 ms pinned-H2D floor).
-    const int nchunks = std::max(1, env_int("BLP_HOST_CHUNKS", 32));
+    // Sub-batches: BLP_HOST_CHUNKS of them (default 16), at least 2048 LPs each, the last ones
+    // tapered (BLP_HOST_TAPER, default 2).  C2 1e5 (round-2 kernels, 13.8 ms pinned-H2D floor):
+    // 16 chunks 14.66 ms uniform / 14.51 tapered; 20: 14.63 / 14.53; 24: 14.84 / 14.57;
+    // 32: 15.0 / 15.0 (round 1, slower kernel: 16 -> 15.2, 32 -> 14.9, 64 -> 15.2).
+    const int nchunks = std::max(1, env_int("BLP_HOST_CHUNKS", 16));
     const long long chunk = std::max<long long>(2048, (count + nchunks - 1) / nchunks);
     const size_t szA = (size_t)m * n, szb = (size_t)m;
 
@@ -905,9 +905,19 @@ int blp_solve_batch_host(const double *A, const double *b, const double *c, int6
         if (rc == BLP_OK) check(cudaEventRecord(shared_ready, ss[0]), "cudaEventRecord");
         for (int k = 1; k < kStreams && rc == BLP_OK; ++k) check(cudaStreamWaitEvent(ss[k], shared_ready, 0), "cudaStreamWaitEvent");
     }
+    // BLP_HOST_TAPER (default 2; 0 = uniform): the last sub-batches halve in size, so the
+    // kernel + D2H after the final H2D is short (the pipeline's drain)
+    const int taper = env_int("BLP_HOST_TAPER", 2);
+    auto sub_size = [&](long long start) -> long long {
+        const long long left = count - start;
+        if (taper <= 0 || left > 2 * chunk) return std::min(chunk, left);
+        const long long half = std::max<long long>(512, left / 2);
+        return std::min(left, std::max<long long>(half, (chunk >> taper)));
+    };
     int ci = 0;
-    for (long long start = 0; start < count && rc == BLP_OK; start += chunk, ++ci) {
-        const long long cnt = std::min(chunk, count - start);
+    long long cnt = 0;
+    for (long long start = 0; start < count && rc == BLP_OK; start += cnt, ++ci) {
+        cnt = sub_size(start);
         cudaStream_t s = ss[ci % kStreams];
         const size_t bytes_in = shared_Ab ? (size_t)cnt * n * 8 : (size_t)cnt * (szA + szb + n) * 8;
         const size_t bytes_out = (size_t)cnt * (n * 8 + 8 + 1 + 8) + 64;
