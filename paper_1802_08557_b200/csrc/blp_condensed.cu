@@ -13,7 +13,8 @@ namespace blp_condensed {
 namespace {
 struct Row { int rpl, ns; Instance inst; };
 // kMinBlocks = resident LPs per SM the register budget is tuned for (C2, ctab_r1_s32:
-// 16 -> 128 registers, 5.05 ms per 1e5; 20 -> 96 registers + spills, 6.37 ms)
+// 16 -> 128 registers, 5.05 ms per 1e5; 14 -> 5.05; 18 -> 112 registers + spills, 6.39;
+// 20 -> 96 registers + spills, 6.37 ms)
 const Row kInstances[] = {
     {1, 8, {blp::condensed_kernel<1, 8, 24>, "ctab_r1_s8", blp::CtCfg<1, 8>::BYTES,
               blp::condensed_phase1_kernel<1, 8>, blp::CtP1<1, 8>::BYTES}},
