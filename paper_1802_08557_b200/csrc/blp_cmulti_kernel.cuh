@@ -8,7 +8,7 @@
 // bookkeeping (states A/B/C, trivial members) is the one-warp kernel's.
 //
 // Layout: thread t holds constraint row t (rows >= m are padding): slots [0, R) in
-// registers, [R, R+S) in a column-major shared tile tile[c][row] with an odd row
+// registers, [R, R+S) in a shared tile of column pairs (tix) with an odd row
 // stride ST >= m, and its rhs; the transposed objective row is dealt one slot per
 // thread (slot q -> thread q: its reduced cost, variable and partner).  Per pivot
 // three CTA barriers separate (A) the per-warp leaving-row partials and the
@@ -26,7 +26,6 @@
 #include "blp_common.cuh"
 #include "blp_condensed_kernel.cuh"
 #include "blp_keys.cuh"
-#include "blp_pairlp_kernel.cuh"
 
 namespace blp {
 
@@ -37,7 +36,8 @@ struct CmCfg {
     static_assert(NS <= ROWS, "one transposed slot per thread");
     static_assert(S == 0 || ((ST & 1) && ST <= ROWS + 1), "odd tile stride, at most one padding row");
     static_assert(R % 2 == 0, "register half in double2 pairs");
-    static constexpr size_t TILE = 0;                                  // S x ST doubles, tile[c][row]
+    static_assert(S % 2 == 0, "tile slots in column pairs");
+    static constexpr size_t TILE = 0;                                  // S x ST doubles, column pairs (tix)
     static constexpr size_t ROWBUF = TILE + (size_t)S * ST * 8;        // 2 x R doubles (double-buffered)
     static constexpr size_t RVEC = ROWBUF + (size_t)2 * R * 8;         // NS (even) doubles
     static constexpr size_t CBV = RVEC + (size_t)((NS + 1) & ~1) * 8;  // ROWS doubles
@@ -78,10 +78,44 @@ struct CmDims { int m, n, nvc, lane, warp, row; };
 __device__ __forceinline__ int cm_cid(int var, int kind, int q) { return (var << 10) | (kind << 8) | q; }
 __device__ __forceinline__ int cm_kind(int cid) { return (cid >> 8) & 3; }
 
+// Tile layout: column pairs, row-major within a pair -- slot c of row r at
+// ((c/2) * ST + r) * 2 + c%2 -- so a row's update moves 16 bytes per access (LDS.128 /
+// STS.128, a warp's 32 rows contiguous: conflict-free) and a column read down the rows
+// (the build, a single slot) stays a plain 8-byte access.
+template <int ST>
+__device__ __forceinline__ size_t tix(int c, int row) { return ((size_t)(c >> 1) * ST + row) * 2 + (c & 1); }
+
 template <int NWR, int R, int S, int ST>
 __device__ __forceinline__ double cm_slot(const CmState<R> &St, const double *tile, int row, int s) {
     if (s < R) return reg_pick<R>(St.a, s);
-    return tile[(size_t)(s - R) * ST + row];
+    return tile[tix<ST>(s - R, row)];
+}
+
+__device__ __forceinline__ void sts_v2_f64(unsigned addr, double x, double y) {
+    asm volatile("st.volatile.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
+// Rank-1 update of this row's tile slots, col pairs p: t -= fs * r, software-pipelined by hand
+// (the tile and rvec share the shared-memory array, so the compiler would serialise each
+// load behind the previous store): pair p+1 and its pivot-row entries load before pair p stores.
+template <int R, int S, int ST>
+__device__ __forceinline__ void cm_update_tile(double *tile, int row, const double *rvec, double fs) {
+    constexpr int NP = S / 2;
+    const unsigned ta = (unsigned)__cvta_generic_to_shared(tile) + 16u * row;
+    const unsigned ra = (unsigned)__cvta_generic_to_shared(rvec + R);
+    double t[2][2], r[2][2];
+    lds_v2_f64(ta, t[0][0], t[0][1]);
+    lds_v2_f64(ra, r[0][0], r[0][1]);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int b = p & 1;
+        if (p + 1 < NP) {
+            lds_v2_f64(ta + 16u * ST * (p + 1), t[b ^ 1][0], t[b ^ 1][1]);
+            lds_v2_f64(ra + 16u * (p + 1), r[b ^ 1][0], r[b ^ 1][1]);
+        }
+        sts_v2_f64(ta + 16u * ST * p, __dsub_rn(t[b][0], __dmul_rn(fs, r[b][0])),
+                   __dsub_rn(t[b][1], __dmul_rn(fs, r[b][1])));
+    }
 }
 
 // Entering candidates of this thread (its slot, its slot's partner, its row's trivial
@@ -159,7 +193,7 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
     if (mine) {
         // slot s then holds the leaving variable's column: e_l, 1 in row l
         if (s < R) rowbuf[s] = 1.0;
-        else tile[(size_t)(s - R) * ST + l] = 1.0;
+        else tile[tix<ST>(s - R, l)] = 1.0;
         X->pe = pe_l;
         X->rr = rr_l;
         X->oldvar = St.basis;
@@ -173,7 +207,7 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
     double newtriv_rc = 0.0;
     const int q = D.row;
     if (q < D.n) {
-        double *src = q < R ? rowbuf + q : tile + (size_t)(q - R) * ST + l;
+        double *src = q < R ? rowbuf + q : tile + tix<ST>(q - R, l);
         const double r = div_entry(*src, pe);
         rvec[q] = r;
         if (q >= R) *src = r;                            // row l of a tile column: final
@@ -204,7 +238,7 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
         const double f = mine ? 0.0 : av;
         St.rhs = mine ? rr : __dsub_rn(St.rhs, __dmul_rn(f, rr));
         if (s < R) reg_put<R>(St.a, s, 0.0);            // the leaving column: e_l
-        else if (!mine) tile[(size_t)(s - R) * ST + D.row] = 0.0;
+        else if (!mine) tile[tix<ST>(s - R, D.row)] = 0.0;
 #pragma unroll
         for (int c = 0; c < R; c += 2) {
             const double2 r2 = reinterpret_cast<const double2 *>(rvec)[c / 2];
@@ -213,7 +247,7 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
         }
         // tile slots: software-pipelined (the tile and rvec share the shared-memory array, so
         // plain loads would serialise behind the previous column's store); row l: r - 0*r, as numpy
-        if constexpr (S > 0) pair_update_tile<R, S, ST>(tile + D.row, rvec, mine ? 0.0 : av);
+        if constexpr (S > 0) cm_update_tile<R, S, ST>(tile, D.row, rvec, mine ? 0.0 : av);
     }
     if ((l >> 5) == D.warp) {        // numpy: r - 0*r == r; warp-uniform reload of row l
         const unsigned rv = (unsigned)__cvta_generic_to_shared(rvec);
@@ -300,7 +334,7 @@ __device__ __forceinline__ void cm_price_out(const CmDims &D, CmState<R> &St, un
         __syncthreads();
         if (live) {
             const int q = D.row;
-            const double v = q < R ? rb[q] : tile[(size_t)(q - R) * ST + r];
+            const double v = q < R ? rb[q] : tile[tix<ST>(q - R, r)];
             racc = __dsub_rn(racc, __dmul_rn(cb, v));
             if (St.spart >= 0) pacc = __dsub_rn(pacc, __dmul_rn(cb, -v));
         }
@@ -342,7 +376,7 @@ __device__ __forceinline__ void cm_restore(const CmDims &D, CmState<R> &St, unsi
         };
         const int q = D.row;
         if (q < D.n) {
-            const double v = fabs(q < R ? rowbuf[q] : tile[(size_t)(q - R) * ST + row]);
+            const double v = fabs(q < R ? rowbuf[q] : tile[tix<ST>(q - R, row)]);
             if (St.svar < D.nvc) consider(v, cm_cid(St.svar, kCtSlot, q));
             if (St.spart >= 0 && St.spart < D.nvc) consider(v, cm_cid(St.spart, kCtPartner, q));
         }
@@ -367,7 +401,7 @@ __device__ __forceinline__ void cm_restore(const CmDims &D, CmState<R> &St, unsi
 #pragma unroll
                 for (int c = 0; c < R; ++c) St.a[c] = -St.a[c];
 #pragma unroll
-                for (int c = 0; c < S; ++c) tile[(size_t)c * ST + row] = -tile[(size_t)c * ST + row];
+                for (int c = 0; c < S; ++c) tile[tix<ST>(c, row)] = -tile[tix<ST>(c, row)];
                 St.rhs = -St.rhs;
                 St.ppart = St.basis;
                 St.basis = j;
@@ -423,7 +457,7 @@ __device__ __forceinline__ bool cm_build(const CmDims &D, CmState<R> &St, unsign
                     nonfinite |= !isfinite(x);
                     v = __dmul_rn(x, sgn);
                 }
-                tile[(size_t)c * ST + D.row] = v;
+                tile[tix<ST>(c, D.row)] = v;
             }
         }
     }
