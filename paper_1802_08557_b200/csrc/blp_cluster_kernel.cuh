@@ -41,7 +41,8 @@
 // differences, IEEE divisions), so results equal theirs and the reference's.
 //
 // The objective value c @ x (simplex.py:190, BLAS ddot in the reference,
-// summation order unpinned) is a 32-lane strided sum here.
+// summation order unpinned) is summed left to right here, as in every kernel and the
+// oracle (a near-zero optimum is ill-conditioned: any other order can miss 1e-9 relative).
 #pragma once
 
 #include "blp_common.cuh"
@@ -806,12 +807,10 @@ cluster_kernel(Batch B) {
             double *xg = B.x + (size_t)lp * n;
             for (int j = X.tid; j < n; j += NT) xg[j] = xs[j];
             if (X.warp == 0) {
+                // c @ x left to right (the oracle's order; see blp_lazy_kernel.cuh)
                 double s = 0.0;
-                if (status == kOptimal) {
-                    for (int j = X.lane; j < n; j += 32) s = __dadd_rn(s, __dmul_rn(cg[j], xs[j]));
-#pragma unroll
-                    for (int off = 16; off; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(kFull, s, off));
-                }
+                if (status == kOptimal && X.lane == 0)
+                    for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(cg[j], xs[j]));
                 if (X.lane == 0) {
                     B.objective[lp] = status == kOptimal ? s : __longlong_as_double(0x7ff8000000000000LL);
                     B.status[lp] = status;

@@ -546,12 +546,12 @@ lazy_kernel(Batch B) {
                 if (basis[i] < n) xg[basis[i]] = rhs[i];
         __syncthreads();
         if (warp == 0) {
+            // c @ x left to right (the oracle's order): a near-zero optimum is a sum of
+            // cancelling terms whose rounding depends on the order (fuzz: condition numbers
+            // up to 1e15 at x ~ 1), so any other order can miss 1e-9 relative
             double s = 0.0;
-            if (status == kOptimal) {
-                for (int j = lane; j < n; j += 32) s = __dadd_rn(s, __dmul_rn(cg[j], xg[j]));
-#pragma unroll
-                for (int off = 16; off; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(kFull, s, off));
-            }
+            if (status == kOptimal && lane == 0)
+                for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(cg[j], xg[j]));
             if (lane == 0) {
                 B.objective[lp] = status == kOptimal ? s : __longlong_as_double(0x7ff8000000000000LL);
                 B.status[lp] = status;
