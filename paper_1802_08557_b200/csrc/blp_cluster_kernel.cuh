@@ -805,12 +805,20 @@ cluster_kernel(Batch B) {
             if (status == kOptimal && X.live && S.basis[X.tid] < n) xs[S.basis[X.tid]] = rhs;
             __syncthreads();
             double *xg = B.x + (size_t)lp * n;
-            for (int j = X.tid; j < n; j += NT) xg[j] = xs[j];
+            for (int j = X.tid; j < n; j += NT) {   // x out; products c_j x_j in place (parallel)
+                const double xj = xs[j];
+                xg[j] = xj;
+                xs[j] = __dmul_rn(cg[j], xj);
+            }
+            __syncthreads();
             if (X.warp == 0) {
                 // c @ x left to right (the oracle's order; see blp_lazy_kernel.cuh)
                 double s = 0.0;
                 if (status == kOptimal && X.lane == 0)
-                    for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(cg[j], xs[j]));
+                    for (int j = 0; j < n; ++j) {
+                        const double p = xs[j];
+                        if (p != 0.0) s = __dadd_rn(s, p);
+                    }
                 if (X.lane == 0) {
                     B.objective[lp] = status == kOptimal ? s : __longlong_as_double(0x7ff8000000000000LL);
                     B.status[lp] = status;

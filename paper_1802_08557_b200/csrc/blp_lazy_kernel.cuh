@@ -536,22 +536,32 @@ lazy_kernel(Batch B) {
             continue;
         }
         // ---- _extract_point (simplex.py:146-151) and c @ x ----
-        double *xs = fcur;                       // reuse: n <= ? -> write x straight to global
-        (void)xs;
+        double *xs = rc;                         // n <= nv doubles, free after the solve
         double *xg = B.x + (size_t)lp * n;
-        for (int j = tid; j < n; j += NT) xg[j] = 0.0;
+        for (int j = tid; j < n; j += NT) xs[j] = 0.0;
         __syncthreads();
         if (status == kOptimal)
             for (int i = tid; i < m; i += NT)
-                if (basis[i] < n) xg[basis[i]] = rhs[i];
+                if (basis[i] < n) xs[basis[i]] = rhs[i];
+        __syncthreads();
+        // c @ x left to right (the oracle's order): a near-zero optimum is a sum of cancelling
+        // terms whose rounding depends on the order (fuzz: condition numbers up to 1e15 at
+        // x ~ 1), so any other order can miss 1e-9 relative.  The products are formed in
+        // parallel (each rounded on its own, as in the sequential loop), the sum by one thread
+        // from shared memory; zero products are skipped (s + 0 == s).
+        for (int j = tid; j < n; j += NT) {
+            const double xj = xs[j];
+            xg[j] = xj;
+            xs[j] = __dmul_rn(cg[j], xj);
+        }
         __syncthreads();
         if (warp == 0) {
-            // c @ x left to right (the oracle's order): a near-zero optimum is a sum of
-            // cancelling terms whose rounding depends on the order (fuzz: condition numbers
-            // up to 1e15 at x ~ 1), so any other order can miss 1e-9 relative
             double s = 0.0;
             if (status == kOptimal && lane == 0)
-                for (int j = 0; j < n; ++j) s = __dadd_rn(s, __dmul_rn(cg[j], xg[j]));
+                for (int j = 0; j < n; ++j) {
+                    const double p = xs[j];
+                    if (p != 0.0) s = __dadd_rn(s, p);
+                }
             if (lane == 0) {
                 B.objective[lp] = status == kOptimal ? s : __longlong_as_double(0x7ff8000000000000LL);
                 B.status[lp] = status;
