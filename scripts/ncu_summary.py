@@ -25,6 +25,7 @@ ap.add_argument("--config", required=True)
 ap.add_argument("--lps", type=int, required=True)
 ap.add_argument("--variant", default=None, help="blp_kernel_variant name (bench.py looks traffic up by it)")
 ap.add_argument("--out", required=True)
+ap.add_argument("--traffic", default="profiles/traffic.json", help="traffic table to update")
 a = ap.parse_args()
 raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -64,7 +65,7 @@ for t in traffic:
     elif "tableau_kernel" in k:
         variant = ("smem" if "(bool)1" in k else "hbm")
     t["variant_family"] = a.variant or variant
-tj = Path("profiles/traffic.json")
+tj = Path(a.traffic)
 recs = json.loads(tj.read_text()) if tj.exists() else []
 for t in traffic:
     # one record per (config, LPs, variant): bench.py looks traffic up by variant
