@@ -308,6 +308,7 @@ void fill_batch(blp::Batch &B, const double *A, const double *b, const double *c
     B.p1state = nullptr;
     B.vq = nullptr;
     B.vflag = nullptr;
+    B.vfirst = 0;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;
@@ -381,6 +382,7 @@ int launch_solve(const double *A, const double *b, const double *c, long long co
     B.p1state = nullptr;
     B.vq = nullptr;
     B.vflag = nullptr;
+    B.vfirst = 0;
     B.lim.max_iterations = lim ? lim->max_iterations : 0;
     B.lim.anti_cycling = lim ? lim->anti_cycling : 1;
     B.lim.degenerate_limit = lim ? lim->degenerate_limit : -1;

@@ -159,6 +159,9 @@ static int lazy_nt(const blp::Batch &B) {
 // lazy_finalize_kernel afterwards.  Measured slower: C5 1e4 5.54 ms vs 5.12 inline, random
 // 100 x 100 2e4 0.91 vs 0.86 -- a solve is a chain of ~5 us pivots, so the CTAs that solve
 // while the others stream are too few; inline, every CTA overlaps its neighbour's stream.
+// BLP_LAZY_SPLIT=2 (every CTA solves first, validation after all solves, so no stream passes
+// through L2 while the replay history is live): 6.09 vs 5.21 ms -- the solves alone take
+// ~3 ms, latency-bound (~6 us per pivot: A and history round trips), with nothing to overlap.
 static bool lazy_split(const blp::Batch &B) {
     return !B.shared_Ab && (long long)B.m * B.n > 0 && !lazy_ws_mode(B, lazy_nt(B)) &&
            env_int("BLP_LAZY_SPLIT", 0) != 0;
@@ -240,6 +243,9 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     const bool split = lazy_split(B);
     Bl.vq = split ? reinterpret_cast<int *>(ws + 128) : nullptr;
     Bl.vflag = split ? flags : nullptr;
+    // BLP_LAZY_SPLIT=1: half the CTAs validate first; 2: every CTA solves first (the solves then
+    // run while no validation stream passes through L2, the validation after them)
+    Bl.vfirst = env_int("BLP_LAZY_SPLIT", 0) == 2 ? 0 : (int)(grid / 2);
     if (split && e == cudaSuccess) e = cudaMemsetAsync(flags, 0, flag_bytes, stream);
     *defer_list = Bl.defer_list;
     *defer_count = Bl.defer_count;

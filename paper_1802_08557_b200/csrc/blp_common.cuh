@@ -71,6 +71,7 @@ struct Batch {
     // Lazy kernel split mode: validation-chunk queue head and per-LP "non-finite A" flags
     int *vq;
     unsigned char *vflag;
+    int vfirst;            // CTAs that take validation chunks before LPs (the rest: LPs first)
 };
 
 // Number of LPs a kernel launch processes, and the batch index of its k-th.

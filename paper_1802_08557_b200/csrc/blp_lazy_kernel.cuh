@@ -242,7 +242,7 @@ lazy_kernel(Batch B) {
     // overlaps the latency-bound solves across CTAs.  A flagged LP is made BLP_STATUS_INVALID
     // by lazy_finalize_kernel after the launch sequence.
     const bool split = !WS && !B.shared_Ab && B.vq != nullptr;
-    const bool validator_first = split && blockIdx.x < gridDim.x / 2;
+    const bool validator_first = split && (int)blockIdx.x < B.vfirst;
     for (;;) {
         if (tid == 0) {
             long long got = B.count;
