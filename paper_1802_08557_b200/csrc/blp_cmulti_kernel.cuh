@@ -227,7 +227,7 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
         St.spart = sp;
     }
     St.obj = __dadd_rn(St.obj, __dmul_rn(fm, rr));       // tableau.py:236-237,242
-    if (CAND) cm_candidates<NWR, R, PH1>(D, St, X, l >= 0 && (l >> 5) == D.warp && mine, newtriv, newtriv_rc);
+    if (CAND) cm_candidates<NWR, R, PH1>(D, St, X, mine, newtriv, newtriv_rc);
     __syncthreads();   // C
     if (mine) {
         St.basis = e;
@@ -254,7 +254,8 @@ __device__ __forceinline__ void cm_pivot(const CmDims &D, CmState<R> &St, unsign
 #pragma unroll
         for (int c = 0; c < R; c += 2) ld_shared_v2_if(mine, rv + 8u * c, St.a[c], St.a[c + 1]);
     }
-    // the next writes to rowbuf / rvec / X come after barrier A of the next pivot
+    // the next writes to rowbuf / rvec / X come after barrier A of the next pivot (X->fm and
+    // the leaving partials: before it, but after every reader has passed barrier C here)
 }
 
 // _run_phase (simplex.py:63-91); entering candidates already in X.

@@ -341,12 +341,14 @@ def test_lazy_tableau_matches_oracle(m, n, monkeypatch):
         compare(_native_dict(got), want, f"lazy {m}x{n} max_iterations={mi}")
 
 
-def test_lazy_split_mode_matches_oracle(monkeypatch):
-    """BLP_LAZY_SPLIT=1 (validation as its own queue) on the single-phase mix, 150 x 150 and
-    100 x 100 (lazy ahead of cmulti): equal to the oracle."""
+@pytest.mark.parametrize("split", ["1", "2"])
+def test_lazy_split_mode_matches_oracle(split, monkeypatch):
+    """BLP_LAZY_SPLIT=1|2 (validation as its own queue; half the CTAs or none validating
+    first) on the single-phase mix, 150 x 150 and 100 x 100 (lazy ahead of cmulti): equal to
+    the oracle."""
     from oracle import oracle
     from paper_1802_08557_b200 import batch_solve_arrays
-    monkeypatch.setenv("BLP_LAZY_SPLIT", "1")
+    monkeypatch.setenv("BLP_LAZY_SPLIT", split)
     for m, n in ((150, 150), (100, 100)):
         A, b, c = _single_phase_mix(m, n, seed=m + 3)
         compare(_native_dict(batch_solve_arrays(A, b, c)), oracle.solve_batch(A, b, c), f"lazy split {m}x{n}")
@@ -400,7 +402,7 @@ def test_lazy_support_staged_replay_matches_plain(monkeypatch):
         assert np.array_equal(r1[k], r2[k], equal_nan=True), k
 
 
-@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("split", ["0", "1", "2"])
 def test_lazy_path_flags_non_finite_entries(split, monkeypatch):
     """A non-finite entry anywhere in A (found by the concurrent validation pass -- inline, or
     the split mode's validation queue + finalize), b or c of a lazy-path batch: that LP comes
