@@ -24,7 +24,9 @@ __device__ __forceinline__ unsigned long long key_max(double v) {
 
 // Key whose unsigned order is numpy's min order: NaN < -inf < ... < +inf.
 __device__ __forceinline__ unsigned long long key_min(double v) {
-    return v != v ? 0ull : key_max(v);
+    const long long b = __double_as_longlong(v == 0.0 ? 0.0 : v);
+    const unsigned long long k = b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+    return v != v ? 0ull : k;   // branch-free, as key_max
 }
 
 constexpr unsigned long long kKeyEmptyMax = 0ull;    // no candidate (max reductions)
