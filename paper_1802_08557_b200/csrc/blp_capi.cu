@@ -680,15 +680,17 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
         // stage this sub-batch's inputs: [A][b][c], packed
         char *p = st.in[k];
         if (src.gather()) {
-            // one memcpy per LP array, LP ranges split over the copy threads
-            char *pA = p, *pb = p + (size_t)cnt * szA * 8, *pc = pb + (size_t)cnt * szb * 8;
+            // one memcpy per LP array, LP ranges split over the copy threads (a shared
+            // polytope: only the objectives)
+            const size_t sa = shared_Ab ? 0 : szA, sb = shared_Ab ? 0 : szb;
+            char *pA = p, *pb = p + (size_t)cnt * sa * 8, *pc = pb + (size_t)cnt * sb * 8;
             const int parts = (int)std::min<long long>(pool.threads(), std::max<long long>(1, cnt / 256));
             pool.parallel_for(parts, [&](int part) {
                 const long long k0 = cnt * part / parts, k1 = cnt * (part + 1) / parts;
                 for (long long q = k0; q < k1; ++q) {
                     const long long lpk = start + q;
-                    if (szA) std::memcpy(pA + (size_t)q * szA * 8, src.Ap[lpk], szA * 8);
-                    if (szb) std::memcpy(pb + (size_t)q * szb * 8, src.bp[lpk], szb * 8);
+                    if (sa) std::memcpy(pA + (size_t)q * sa * 8, src.Ap[lpk], sa * 8);
+                    if (sb) std::memcpy(pb + (size_t)q * sb * 8, src.bp[lpk], sb * 8);
                     if (n) std::memcpy(pc + (size_t)q * n * 8, src.cp[lpk], (size_t)n * 8);
                 }
             });
@@ -980,7 +982,14 @@ int blp_solve_batch_gather(const double *const *A, const double *const *b, const
     if (rc != BLP_OK) return rc;
     InputSource src;
     src.Ap = A; src.bp = b; src.cp = c;
-    return solve_host_staged(src, count, m, n, 0, limits, status, objective, x, iters1, iters2, device,
+    // Every LP pointing at the same A and b (the support-function workload through the
+    // reference's list API: one polytope object, many objectives): solved in support mode --
+    // the polytope uploaded once, its phase 1 shared -- with outputs identical to solving
+    // each LP on its own (tests/test_gpu_support_phase1.py).  BLP_GATHER_SHARED=0 disables.
+    bool shared = env_int("BLP_GATHER_SHARED", 1) != 0;
+    for (long long k = 1; k < count && shared; ++k) shared = A[k] == A[0] && b[k] == b[0];
+    if (shared) { src.A = A[0]; src.b = b[0]; }
+    return solve_host_staged(src, count, m, n, shared ? 1 : 0, limits, status, objective, x, iters1, iters2, device,
                              g_streams[device].s);
 }
 

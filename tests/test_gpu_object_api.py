@@ -136,3 +136,23 @@ def test_two_rank_bench_on_one_gpu():
     assert pr["checked"] == 10_000 and pr["of"] == 40_000
     assert pr["status_mismatch"] == pr["x_mismatch"] == pr["iter_mismatch"] == 0 and pr["max_obj_rel"] <= 1e-9
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] >= 3
+
+
+def test_object_api_shared_polytope_is_support_mode(monkeypatch):
+    """LPs of a list that all point at one A and one b (the support-function workload through
+    the reference API) are solved in support mode -- phase 1 shared -- with outputs equal to
+    the oracle's per-LP solves and to the library's per-LP path (BLP_GATHER_SHARED=0);
+    equal-valued but distinct arrays take the per-LP path."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import StandardFormLP, batch_solve, workloads
+    A, b = workloads.support_polytope_two_phase()
+    C = workloads.support_directions(4000, offset=9)
+    lps = [StandardFormLP(c=C[k], A=A, b=b) for k in range(len(C))]
+    want = oracle.solve_batch(A, b, C, shared_Ab=True, threads=oracle.host_cores())
+    compare(_arrays_of(batch_solve(lps)), want, "object api shared two-phase polytope")
+    monkeypatch.setenv("BLP_GATHER_SHARED", "0")
+    compare(_arrays_of(batch_solve(lps)), want, "object api shared polytope, per-LP path")
+    monkeypatch.delenv("BLP_GATHER_SHARED")
+    lps2 = [StandardFormLP(c=C[k], A=A.copy(), b=b.copy()) for k in range(300)]
+    compare(_arrays_of(batch_solve(lps2)), {k: v[:300] for k, v in want.items() if k != "threads"},
+            "object api distinct copies")
