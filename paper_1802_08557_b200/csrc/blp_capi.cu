@@ -579,6 +579,8 @@ bool is_pinned(const void *p) {
 struct Staging {
     char *in[4] = {}, *out[4] = {};
     size_t in_bytes = 0, out_bytes = 0;
+    char *poly = nullptr;          // pinned copy of a shared polytope (support mode), reused
+    size_t poly_bytes = 0;
 };
 Staging g_staging[64];
 std::mutex g_staging_mu[64];
@@ -623,12 +625,24 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
     }
     // Shared polytope: uploaded once on ss[0] through pinned slot 0 (a pageable source
     // would let cudaMemcpy return before the DMA lands), and every stream waits for it.
+    // The pinned copy is a per-device buffer reused across calls (pinning pages per call cost
+    // ~ms: the reference's list API makes one call per planned chunk, 49 for C4), and the
+    // device copy is stream-ordered (cudaMallocAsync / cudaFreeAsync on ss[0]): calls on a
+    // device are serialised by the staging mutex and drain every stream before returning.
     double *dA_shared = nullptr, *db_shared = nullptr;
     if (shared_Ab) {
-        BLP_CUDA_TRY(cudaMalloc(&dA_shared, std::max<size_t>(1, szA) * 8));
-        BLP_CUDA_TRY(cudaMalloc(&db_shared, std::max<size_t>(1, szb) * 8));
-        char *hp = nullptr;
-        BLP_CUDA_TRY(cudaMallocHost(reinterpret_cast<void **>(&hp), (szA + szb) * 8 + 16));
+        const size_t pbytes = (szA + szb) * 8 + 16;
+        if (st.poly_bytes < pbytes) {
+            if (st.poly) cudaFreeHost(st.poly);
+            st.poly = nullptr;
+            st.poly_bytes = 0;
+            BLP_CUDA_TRY(cudaMallocHost(reinterpret_cast<void **>(&st.poly), pbytes));
+            st.poly_bytes = pbytes;
+        }
+        char *hp = st.poly;
+        BLP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&dA_shared), (std::max<size_t>(1, szA) + std::max<size_t>(1, szb)) * 8,
+                                     ss[0]));
+        db_shared = dA_shared + std::max<size_t>(1, szA);
         if (szA) std::memcpy(hp, A, szA * 8);
         if (szb) std::memcpy(hp + szA * 8, b, szb * 8);
         cudaError_t e = cudaSuccess;
@@ -639,13 +653,12 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
         if (e == cudaSuccess) {
             e = cudaEventRecord(up, ss[0]);
             for (int k = 1; k < kSlots && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ss[k], up, 0);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(ss[0]);   // hp is freed below
             cudaEventDestroy(up);
         }
-        cudaFreeHost(hp);
         if (e != cudaSuccess) {
-            cudaFree(dA_shared);
-            cudaFree(db_shared);
+            cudaStreamSynchronize(ss[0]);
+            cudaFreeAsync(dA_shared, ss[0]);
+            cudaStreamSynchronize(ss[0]);
             return fail(BLP_ERR_CUDA, std::string("shared polytope upload: ") + cudaGetErrorString(e));
         }
     }
@@ -740,8 +753,10 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
         if (e != cudaSuccess && rc == BLP_OK) rc = fail(BLP_ERR_CUDA, cudaGetErrorString(e));
         cudaEventDestroy(ev[k]);
     }
-    if (dA_shared) cudaFree(dA_shared);
-    if (db_shared) cudaFree(db_shared);
+    if (dA_shared) {                         // every stream drained above
+        cudaFreeAsync(dA_shared, ss[0]);
+        cudaStreamSynchronize(ss[0]);
+    }
     return rc;
 }
 
