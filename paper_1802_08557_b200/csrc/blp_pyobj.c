@@ -73,6 +73,7 @@ static PyObject *collect(PyObject *self, PyObject *args) {
     int64_t *P = (int64_t *)PyBytes_AS_STRING(ptrs);
     int64_t *PA = P, *Pb = P + count, *Pc = P + 2 * count;
     long worst_neg = 0;
+    const double *last_pb = NULL;
     Py_ssize_t first_hetero = -1;
     for (Py_ssize_t k = 0; k < count; ++k) {
         PyObject *lp = items[k];
@@ -112,9 +113,12 @@ static PyObject *collect(PyObject *self, PyObject *args) {
             PA[k] = (int64_t)(intptr_t)pA;
             Pb[k] = (int64_t)(intptr_t)pb;
             Pc[k] = (int64_t)(intptr_t)pc;
-            long neg = 0;
-            for (Py_ssize_t i = 0; i < m; ++i) neg += pb[i] < 0.0;
-            if (neg > worst_neg) worst_neg = neg;
+            if (pb != last_pb) {   /* one shared b (support function): counted once */
+                long neg = 0;
+                for (Py_ssize_t i = 0; i < m; ++i) neg += pb[i] < 0.0;
+                if (neg > worst_neg) worst_neg = neg;
+                last_pb = pb;
+            }
         }
         Py_DECREF(A);
         Py_DECREF(b);
