@@ -545,7 +545,8 @@ def test_results_invariant_to_chunking_and_sharding(monkeypatch):
     c = np.concatenate([c1, c2[:, :40]])
     ref = _native_dict(batch_solve_arrays(A, b, c))
     variants = [dict(BLP_HOST_CHUNKS="3"), dict(BLP_HOST_CHUNKS="64"), dict(BLP_HOST_TAPER="0"),
-                dict(BLP_HOST_CHUNKS="5", BLP_HOST_TAPER="6"), dict(BLP_STAGE_MB="1"), dict(BLP_STAGE="0")]
+                dict(BLP_HOST_CHUNKS="5", BLP_HOST_TAPER="6"), dict(BLP_HOST_RAMP="0"), dict(BLP_HOST_RAMP="6"),
+                dict(BLP_STAGE_MB="1"), dict(BLP_STAGE="0")]
     for env in variants:
         for k, v in env.items():
             monkeypatch.setenv(k, v)
