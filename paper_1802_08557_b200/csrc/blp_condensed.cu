@@ -38,9 +38,9 @@ const Row kInstances[] = {
 
 // Multi-warp condensed form (blp_cmulti_kernel.cuh): NWR row-warps, R register slots and S
 // tile slots per row, tile stride ST (odd, >= m), kMinBlocks LPs per SM.
-struct MRow { int nwr, ns, r; Instance inst; };
+struct MRow { int nwr, ns, r, st; Instance inst; };
 #define CM_INST(NWR, R, S, ST, MB)                                                                     \
-    {NWR, R + S, R, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
+    {NWR, R + S, R, ST, {blp::cmulti_kernel<NWR, R, S, ST, MB>, "cm" #NWR "_r" #R "_s" #S,                  \
                   blp::CmCfg<NWR, R, S, ST>::BYTES, blp::cmulti_phase1_kernel<NWR, R, S, ST>,                \
                   blp::CmP1<NWR, R, S, ST>::BYTES, 32 * NWR}}
 // First fit in this order.  C3 (100 x 100, c3 count 2e4, device-resident): r48_s56 at 3 LPs
@@ -83,7 +83,7 @@ bool select(int m, int n, Instance *out) {
         if (cm == 2 || m > 64 || !one_warp_fits) {
             const int want_r = env_int("BLP_CM_R", 0);
             for (const MRow &r : kMulti) {
-                if (r.nwr != nwr || n > r.ns) continue;
+                if (r.nwr != nwr || n > r.ns || m > r.st) continue;
                 if (want_r && r.r != want_r) continue;
                 *out = r.inst;
                 return true;

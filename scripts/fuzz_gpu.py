@@ -43,18 +43,33 @@ def recipe(rng, m, n, cnt, seed):
     return np.ascontiguousarray(A), np.ascontiguousarray(b), np.ascontiguousarray(c)
 
 
-def run(seed: int, seconds: float | None = None, cases: int | None = None, log=print) -> tuple[int, int, int]:
-    """Random cases until the time or case budget is spent; returns (cases, LPs, mismatches)."""
+def run(seed: int, seconds: float | None = None, cases: int | None = None, log=print,
+        huge: bool = False) -> tuple[int, int, int]:
+    """Random cases until the time or case budget is spent; returns (cases, LPs, mismatches).
+    huge: 400..700 rows/columns (the lazy, cluster and HBM-streamed families), single-phase
+    random LPs and the degenerate recipe only (two-phase LPs of that size take the oracle
+    minutes)."""
     rng = np.random.default_rng(seed)
     t_end = time.time() + seconds if seconds is not None else None
     done = bad = lps = 0
     while (t_end is None or time.time() < t_end) and (cases is None or done < cases):
         big = rng.random() < 0.1
-        m = int(rng.integers(1, 300 if big else 140))
-        n = int(rng.integers(1, 300 if big else 140))
-        cnt = int(rng.integers(1, 8 if big else 120))
+        if huge:
+            m, n, cnt = int(rng.integers(400, 701)), int(rng.integers(400, 701)), int(rng.integers(1, 4))
+        else:
+            m = int(rng.integers(1, 300 if big else 140))
+            n = int(rng.integers(1, 300 if big else 140))
+            cnt = int(rng.integers(1, 8 if big else 120))
         seed_k = int(rng.integers(1 << 30))
-        A, b, c = recipe(rng, m, n, cnt, seed_k)
+        if huge:
+            if rng.random() < 0.5:
+                A, b, c = workloads.random_arrays(max(m, n), cnt, seed_k)
+                A, b, c = (np.ascontiguousarray(v) for v in (A[:, :m, :n], b[:, :m], c[:, :n]))
+            else:
+                A, b, c = workloads.degenerate_arrays(cnt, seed=seed_k, m=m, n=n)
+                b = np.abs(b)
+        else:
+            A, b, c = recipe(rng, m, n, cnt, seed_k)
         shared = rng.random() < 0.2
         if shared:
             A, b = A[0].copy(), b[0].copy()
@@ -95,7 +110,8 @@ if __name__ == "__main__":
     p = argparse.ArgumentParser()
     p.add_argument("--seconds", type=float, default=300)
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--huge", action="store_true", help="400..700-sized single-phase / degenerate LPs")
     a = p.parse_args()
-    cases, lps, bad = run(a.seed, seconds=a.seconds, log=lambda s: print(s, flush=True))
+    cases, lps, bad = run(a.seed, seconds=a.seconds, log=lambda s: print(s, flush=True), huge=a.huge)
     print(f"fuzz: {cases} cases, {lps} LPs, {bad} mismatches", flush=True)
     sys.exit(1 if bad else 0)
