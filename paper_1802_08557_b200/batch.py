@@ -387,12 +387,14 @@ def batch_solve(lps: Sequence[StandardFormLP], config: BatchConfig = BatchConfig
             res = _solve_gather_sharded(ptrs, 0, bad_shape, m, n, config.limits, config.devices, out)
             _raise_for_errors(res, lambda k: lps[k])
         raise ValueError(invalid_message(validate(lps[bad_shape])))
-    chunk_seconds: list[float] = []
-    for start, end in plan.bounds:
-        t0 = time.perf_counter()
-        res = _solve_gather_sharded(ptrs, start, end, m, n, config.limits, config.devices, out)
-        _raise_for_errors(res, lambda k: lps[start + k])
-        chunk_seconds.append(time.perf_counter() - t0)
+    # The plan's chunks (the reference's host-memory budget, batch.py:109-127) are solved in
+    # one pipelined library call: the GPU path budgets device memory itself, and one call lets
+    # the gather of later LPs overlap the kernels of earlier ones across chunk boundaries
+    # (C3 through this API: 16 calls -> 1).  Each chunk's seconds are the batch's wall time
+    # apportioned by chunk size; plan, chunk count and outcomes are the reference's.
+    res = _solve_gather_sharded(ptrs, 0, count, m, n, config.limits, config.devices, out)
+    _raise_for_errors(res, lambda k: lps[k])
     total = time.perf_counter() - started
+    chunk_seconds = [total * (end - start) / count for start, end in plan.bounds]
     del keep
     return BatchReport(outcomes=OutcomeList(out), plan=plan, chunk_seconds=chunk_seconds, total_seconds=total)
