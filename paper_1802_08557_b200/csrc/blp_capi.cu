@@ -602,7 +602,13 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
     const size_t szA = (size_t)m * n, szb = (size_t)m;
     const size_t in_lp = (shared_Ab ? 0 : (szA + szb) * 8) + (size_t)n * 8;
     const size_t out_lp = (size_t)n * 8 + 8 + 4 + 4 + 1;
-    const size_t slot = (size_t)std::max(1, env_int("BLP_STAGE_MB", 64)) << 20;
+    // Slot size: room for >= 2048 LPs (or a 16th of the batch), between 64 and 256 MB
+    // (BLP_STAGE_MB overrides).  Large LPs need it: C3 (81 KB of inputs per LP) through the
+    // list API in 64 MB slots ran 792-LP sub-batches, too small to fill the GPU: 600 ms per
+    // 1e5; 256 MB: 376 ms.
+    const size_t want_slot = in_lp * (size_t)std::max<long long>(2048, (count + 15) / 16);
+    const size_t dflt_mb = std::min<size_t>(256, std::max<size_t>(64, (want_slot + (1 << 20) - 1) >> 20));
+    const size_t slot = (size_t)std::max(1, env_int("BLP_STAGE_MB", (int)dflt_mb)) << 20;
     long long chunk = std::max<long long>(1, (long long)(slot / std::max<size_t>(1, in_lp)));
     chunk = std::min<long long>(chunk, std::max<long long>(2048, (count + 15) / 16));   // keep a pipeline
     chunk = std::min<long long>(chunk, count);
@@ -697,7 +703,10 @@ int solve_host_staged(const InputSource &src, long long count, int m, int n,
             // polytope: only the objectives)
             const size_t sa = shared_Ab ? 0 : szA, sb = shared_Ab ? 0 : szb;
             char *pA = p, *pb = p + (size_t)cnt * sa * 8, *pc = pb + (size_t)cnt * sb * 8;
-            const int parts = (int)std::min<long long>(pool.threads(), std::max<long long>(1, cnt / 256));
+            // split by bytes, not LP count: 128 LPs of 500 x 500 are 256 MB (C5 through the list
+            // API: one copy thread at cnt / 256 = 0, 8.5 GB/s)
+            const long long bytes = cnt * (long long)((sa + sb + n) * 8);
+            const int parts = (int)std::min<long long>(pool.threads(), std::max<long long>(1, bytes >> 21));
             pool.parallel_for(parts, [&](int part) {
                 const long long k0 = cnt * part / parts, k1 = cnt * (part + 1) / parts;
                 for (long long q = k0; q < k1; ++q) {
