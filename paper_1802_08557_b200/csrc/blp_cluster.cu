@@ -250,11 +250,12 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     *defer_list = Bl.defer_list;
     *defer_count = Bl.defer_count;
     if (e == cudaSuccess) {
-        // BLP_LAZY_PERSIST (pivots, 0 = off): the first pivots' replay history of every resident
-        // CTA -- one contiguous range in the pivot-major layout -- is marked persisting in L2, so
-        // the validation stream of A passing through L2 does not evict it between the replays
-        // that re-read it (ncu, C5: 8.2 GB of the history/column re-reads missed L2 without).
-        const int kp = B.shared_Ab ? 0 : env_int("BLP_LAZY_PERSIST", 16);
+        // BLP_LAZY_PERSIST (pivots; default 0 = off): the first pivots' replay history of every
+        // resident CTA -- one contiguous range in the pivot-major layout -- is marked persisting
+        // in L2 against the validation stream of A.  Measured within noise (C5 5.19 vs 5.22 ms
+        // alternating in one process; ncu: the same L2 read misses with and without), and it
+        // raises the device-wide persisting-L2 limit, so it is opt-in.
+        const int kp = B.shared_Ab ? 0 : env_int("BLP_LAZY_PERSIST", 0);
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         cfg.gridDim = dim3((unsigned)grid);
