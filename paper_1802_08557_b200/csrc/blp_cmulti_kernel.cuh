@@ -1,5 +1,6 @@
 // blp_cmulti_kernel.cuh -- the condensed tableau (blp_condensed_kernel.cuh) on one
-// CTA of NWR row-warps per LP, for 33..128 constraint rows (C3, 100 x 100: NWR = 4).
+// CTA of NWR row-warps per LP, for 33..256 constraint rows (C4 64 x 32: NWR = 2; C3,
+// 100 x 100: NWR = 4; 129..256 rows: NWR = 8, one LP per SM).
 //
 // Same exactness argument as the one-warp kernel: only the n nonbasic columns and
 // the rhs are stored and updated -- a basic column is exactly e_r and the reference
@@ -31,6 +32,7 @@ namespace blp {
 
 template <int NWR, int R, int S, int ST>
 struct CmCfg {
+    static_assert(NWR == 2 || NWR == 4 || NWR == 8, "row-warps per LP");
     static constexpr int NS = R + S;                 // nonbasic slots per row
     static constexpr int ROWS = 32 * NWR;
     static_assert(NS <= ROWS, "one transposed slot per thread");
@@ -49,12 +51,12 @@ struct CmCfg {
 
 // Per-pivot exchange between the warps.
 struct CmXch {
-    unsigned long long ckey[4];    // entering candidates per warp (Dantzig key, composite id)
-    int cid[4];
-    int cbl[4];                    // Bland: lowest composite id with rc > tol
-    unsigned long long lkey[4];    // leaving partials per warp
-    int lrow[4];
-    int nneg[4];                   // negated rows per warp (artificial numbering)
+    unsigned long long ckey[8];    // entering candidates per warp (Dantzig key, composite id)
+    int cid[8];
+    int cbl[8];                    // Bland: lowest composite id with rc > tol
+    unsigned long long lkey[8];    // leaving partials per warp
+    int lrow[8];
+    int nneg[8];                   // negated rows per warp (artificial numbering)
     int nonfinite;
     long long lp;                  // the LP the CTA solves next
     double pe, fm, rr, oldprc, newtriv_rc;

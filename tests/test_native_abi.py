@@ -42,7 +42,7 @@ def test_host_only_entry_points():
                                         (100, 100, "lazy+cm4_r48_s56"), (50, 50, "lazy+cm2_r64_s0"), (100, 150, "lazy+smem"),
                                         (90, 140, "lazy+smem"), (64, 40, "lazy+cm2_r64_s0"),
                                         (500, 500, "lazy+cluster"),
-                                        (150, 150, "lazy+cluster"), (600, 600, "lazy+hbm")])
+                                        (150, 150, "lazy+cm8_r96_s104"), (300, 150, "lazy+cluster"), (600, 600, "lazy+hbm")])
 def test_kernel_variant_selection(m, n, family):
     assert _native.kernel_variant(m, n).startswith(family)
 
