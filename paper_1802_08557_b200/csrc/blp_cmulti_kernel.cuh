@@ -32,7 +32,7 @@ namespace blp {
 
 template <int NWR, int R, int S, int ST>
 struct CmCfg {
-    static_assert(NWR == 2 || NWR == 4 || NWR == 8, "row-warps per LP");
+    static_assert(NWR == 2 || NWR == 4 || NWR == 8 || NWR == 16, "row-warps per LP");
     static constexpr int NS = R + S;                 // nonbasic slots per row
     static constexpr int ROWS = 32 * NWR;
     static_assert(NS <= ROWS, "one transposed slot per thread");
@@ -46,17 +46,17 @@ struct CmCfg {
     static constexpr size_t RHSV = CBV + (size_t)ROWS * 8;             // ROWS doubles
     static constexpr size_t FLAG = RHSV + (size_t)ROWS * 8;            // ROWS ints
     static constexpr size_t XCH = FLAG + (size_t)ROWS * 4;
-    static constexpr size_t BYTES = XCH + 512;
+    static constexpr size_t BYTES = XCH + 768;
 };
 
-// Per-pivot exchange between the warps.
+// Per-pivot exchange between the warps (768 bytes reserved).
 struct CmXch {
-    unsigned long long ckey[8];    // entering candidates per warp (Dantzig key, composite id)
-    int cid[8];
-    int cbl[8];                    // Bland: lowest composite id with rc > tol
-    unsigned long long lkey[8];    // leaving partials per warp
-    int lrow[8];
-    int nneg[8];                   // negated rows per warp (artificial numbering)
+    unsigned long long ckey[16];   // entering candidates per warp (Dantzig key, composite id)
+    int cid[16];
+    int cbl[16];                   // Bland: lowest composite id with rc > tol
+    unsigned long long lkey[16];   // leaving partials per warp
+    int lrow[16];
+    int nneg[16];                  // negated rows per warp (artificial numbering)
     int nonfinite;
     long long lp;                  // the LP the CTA solves next
     double pe, fm, rr, oldprc, newtriv_rc;

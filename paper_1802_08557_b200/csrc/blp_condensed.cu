@@ -58,6 +58,8 @@ const MRow kMulti[] = {
     CM_INST(8, 24, 40, 257, 2),
     CM_INST(8, 64, 64, 257, 1),
     CM_INST(8, 96, 104, 257, 1),
+    // 257..512 rows, n <= 72: sixteen row-warps
+    CM_INST(16, 24, 48, 513, 1),
     // A/B alternatives (BLP_CM_R selects the register width)
     CM_INST(4, 88, 16, 129, 2),
     CM_INST(4, 80, 24, 129, 2),
@@ -81,8 +83,8 @@ bool select(int m, int n, Instance *out) {
     // 2 (default) for every 33..128-row shape (C4 64 x 32, 2e5 directions: cm2_r32_s0 7.88 ms,
     // the one-warp ctab_r2_s32 8.71)
     const int cm = env_int("BLP_CMULTI", 2);
-    if (m > 32 && m <= 256 && cm != 0) {
-        const int nwr = m <= 64 ? 2 : (m <= 128 ? 4 : 8);
+    if (m > 32 && m <= 512 && cm != 0) {
+        const int nwr = m <= 64 ? 2 : (m <= 128 ? 4 : (m <= 256 ? 8 : 16));
         const bool one_warp_fits = (m <= 64 && n <= 32) || (m > 64 && n <= 16);
         if (cm == 2 || m > 64 || !one_warp_fits) {
             const int want_r = env_int("BLP_CM_R", 0);

@@ -47,7 +47,7 @@ def test_c4b_directions_match_oracle():
 
 @pytest.mark.parametrize("cm", ["0", "2"])
 @pytest.mark.parametrize("m,n", [(20, 12), (28, 32), (40, 16), (64, 8), (100, 12), (64, 32), (100, 100), (120, 128),
-                                 (160, 48), (220, 150)])
+                                 (160, 48), (220, 150), (400, 60)])
 def test_shared_phase1_every_condensed_shape(m, n, cm, monkeypatch):
     """Every condensed instance family -- one warp (rows per lane 1/2/4; BLP_CMULTI=0) and
     multi-warp (cmulti, registers + tile; BLP_CMULTI=2) -- with a mixed-sign shared b:
