@@ -199,13 +199,19 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
     size_t smem = blp::lazy_smem_bytes(B.m, B.n, ws_mode, threads, rp);
     // BLP_LAZY_FSMEM=1: f^t history of the first pivots in shared memory (two CTAs per SM kept)
     // (value > 1: per-CTA shared-memory cap in KB; 1: 113 KB)
-    const int fsmem = env_int("BLP_LAZY_FSMEM", 0);
-    if (nt == 512 && !ws_mode && !rp && fsmem) {
-        const size_t base = (smem + 15) / 16 * 16, cap = (size_t)(fsmem > 1 ? fsmem : 113) * 1024;
-        const size_t kf = base < cap ? std::min<size_t>(blp::kLazyMaxPivots, (cap - base) / (8 * (size_t)std::max(1, B.m))) : 0;
-        if (kf >= 4) {
-            fn = (LazyFn)blp::lazy_kernel<512, 2, 0, 0, 1>;
-            smem = base + kf * 8 * (size_t)B.m;
+    // BLP_LAZY_RSMEM=1: the r^t history of those pivots too (same cap semantics).  Measured
+    // (C5 1e4, parity-checked): default 5.39 ms; FSMEM=1 8.04; RSMEM=1 8.26, =100 6.14, =80
+    // 5.94 -- the history bytes taken off L2 cost L1 capacity (the entering column's strided
+    // reads of A hit there) and residency, so both stay opt-in.
+    const int fsmem = env_int("BLP_LAZY_FSMEM", 0), rsmem = env_int("BLP_LAZY_RSMEM", 0);
+    if (nt == 512 && !ws_mode && !rp && (fsmem || rsmem)) {
+        const int capk = rsmem > 1 ? rsmem : fsmem > 1 ? fsmem : 113;
+        const size_t base = (smem + 15) / 16 * 16, cap = (size_t)capk * 1024;
+        const size_t per = 8 * (size_t)std::max(1, B.m) + (rsmem ? 8 * (size_t)(B.n + B.m) : 0);
+        const size_t kf = base < cap ? std::min<size_t>(blp::kLazyMaxPivots, (cap - base) / per) : 0;
+        if (kf >= (rsmem ? 2u : 4u)) {
+            fn = rsmem ? (LazyFn)blp::lazy_kernel<512, 2, 0, 0, 2> : (LazyFn)blp::lazy_kernel<512, 2, 0, 0, 1>;
+            smem = base + kf * per;
         }
     }
     *ws_out = nullptr;

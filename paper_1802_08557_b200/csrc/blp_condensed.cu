@@ -11,29 +11,29 @@
 namespace blp_condensed {
 
 namespace {
-struct Row { int rpl, ns; Instance inst; };
+struct Row { int rpl, ns; Instance inst; size_t stg_end; };
 // kMinBlocks = resident LPs per SM the register budget is tuned for (C2, ctab_r1_s32:
 // 16 -> 128 registers, 5.05 ms per 1e5; 14 -> 5.05; 18 -> 112 registers + spills, 6.39;
 // 20 -> 96 registers + spills, 6.37 ms)
 const Row kInstances[] = {
     {1, 8, {blp::condensed_kernel<1, 8, 24>, "ctab_r1_s8", blp::CtCfg<1, 8>::BYTES,
-              blp::condensed_phase1_kernel<1, 8>, blp::CtP1<1, 8>::BYTES}},
+              blp::condensed_phase1_kernel<1, 8>, blp::CtP1<1, 8>::BYTES}, blp::CtCfg<1, 8>::STG_END},
     {1, 16, {blp::condensed_kernel<1, 16, 20>, "ctab_r1_s16", blp::CtCfg<1, 16>::BYTES,
-              blp::condensed_phase1_kernel<1, 16>, blp::CtP1<1, 16>::BYTES}},
+              blp::condensed_phase1_kernel<1, 16>, blp::CtP1<1, 16>::BYTES}, blp::CtCfg<1, 16>::STG_END},
     {1, 32, {blp::condensed_kernel<1, 32, 16>, "ctab_r1_s32", blp::CtCfg<1, 32>::BYTES,
-              blp::condensed_phase1_kernel<1, 32>, blp::CtP1<1, 32>::BYTES}},
+              blp::condensed_phase1_kernel<1, 32>, blp::CtP1<1, 32>::BYTES}, blp::CtCfg<1, 32>::STG_END},
     {1, 64, {blp::condensed_kernel<1, 64, 8>, "ctab_r1_s64", blp::CtCfg<1, 64>::BYTES,
-              blp::condensed_phase1_kernel<1, 64>, blp::CtP1<1, 64>::BYTES}},
+              blp::condensed_phase1_kernel<1, 64>, blp::CtP1<1, 64>::BYTES}, blp::CtCfg<1, 64>::STG_END},
     {2, 8, {blp::condensed_kernel<2, 8, 12>, "ctab_r2_s8", blp::CtCfg<2, 8>::BYTES,
-              blp::condensed_phase1_kernel<2, 8>, blp::CtP1<2, 8>::BYTES}},
+              blp::condensed_phase1_kernel<2, 8>, blp::CtP1<2, 8>::BYTES}, blp::CtCfg<2, 8>::STG_END},
     {2, 16, {blp::condensed_kernel<2, 16, 10>, "ctab_r2_s16", blp::CtCfg<2, 16>::BYTES,
-              blp::condensed_phase1_kernel<2, 16>, blp::CtP1<2, 16>::BYTES}},
+              blp::condensed_phase1_kernel<2, 16>, blp::CtP1<2, 16>::BYTES}, blp::CtCfg<2, 16>::STG_END},
     {2, 32, {blp::condensed_kernel<2, 32, 8>, "ctab_r2_s32", blp::CtCfg<2, 32>::BYTES,
-              blp::condensed_phase1_kernel<2, 32>, blp::CtP1<2, 32>::BYTES}},
+              blp::condensed_phase1_kernel<2, 32>, blp::CtP1<2, 32>::BYTES}, blp::CtCfg<2, 32>::STG_END},
     {4, 8, {blp::condensed_kernel<4, 8, 10>, "ctab_r4_s8", blp::CtCfg<4, 8>::BYTES,
-              blp::condensed_phase1_kernel<4, 8>, blp::CtP1<4, 8>::BYTES}},
+              blp::condensed_phase1_kernel<4, 8>, blp::CtP1<4, 8>::BYTES}, blp::CtCfg<4, 8>::STG_END},
     {4, 16, {blp::condensed_kernel<4, 16, 8>, "ctab_r4_s16", blp::CtCfg<4, 16>::BYTES,
-              blp::condensed_phase1_kernel<4, 16>, blp::CtP1<4, 16>::BYTES}},
+              blp::condensed_phase1_kernel<4, 16>, blp::CtP1<4, 16>::BYTES}, blp::CtCfg<4, 16>::STG_END},
 };
 
 // Multi-warp condensed form (blp_cmulti_kernel.cuh): NWR row-warps, R register slots and S
@@ -100,6 +100,12 @@ bool select(int m, int n, Instance *out) {
     for (const Row &r : kInstances) {
         if (r.rpl != rpl || n > r.ns) continue;
         *out = r.inst;
+        // BLP_CT_STAGE: grant the TMA staging buffer of the next LP's A -- 1 (default) for rows
+        // of >= 32 doubles, 2 always, 0 never.  Measured (1e5 LPs, staged vs direct loads): C2
+        // 28 x 32 4.945 vs 4.997 ms; afiro 20 x 10 (ctab_r1_s16) 1.409 vs 1.348; 64 x 16
+        // (ctab_r2_s16) 11.05 vs 10.86 -- short rows make many small bulk copies per LP.
+        const int stage = env_int("BLP_CT_STAGE", 1);
+        if (stage == 2 || (stage == 1 && n >= 32)) out->smem = r.stg_end;
         return true;
     }
     return false;

@@ -52,6 +52,12 @@ struct CtCfg {
     static constexpr size_t RHSV = CBV + (size_t)32 * RPL * 8;
     static constexpr size_t XS = RHSV + (size_t)32 * RPL * 8;  // NS doubles: x scatter
     static constexpr size_t BYTES = XS + (size_t)NS * 8;
+    // Optional TMA staging of the next LP's A (condensed_kernel, when the launch grants
+    // STG_END bytes): an mbarrier, then 32*RPL rows at a stride of NS*8 + 16 bytes (16-byte
+    // aligned for cp.async.bulk; lane L's 128-bit row reads spread over 8 bank groups).
+    static constexpr size_t STG_BAR = (BYTES + 15) / 16 * 16;
+    static constexpr size_t STG = STG_BAR + 16;
+    static constexpr size_t STG_END = STG + (size_t)32 * RPL * (NS * 8 + 16);
 };
 
 template <int RPL, int NS>
@@ -480,9 +486,10 @@ __device__ __forceinline__ void ct_restore(const CtDims &D, CtState<RPL, NS> &S,
 // build_tableau (tableau.py:139-172): rows straight into their lane, validation fused
 // (a non-finite A, b or c entry sets `nonfinite`); slot q starts as structural x_q with
 // reduced cost c_q (0 without c: the shared phase-1 prologue).  Returns n_art.
-template <int RPL, int NS>
+template <int RPL, int NS, bool V2 = false>
 __device__ __forceinline__ int ct_build(const CtDims &D, CtState<RPL, NS> &S, const double *Ag, const double *bg,
-                                        const double *cg, bool &nonfinite) {
+                                        const double *cg, bool &nonfinite, int lda = -1) {
+    if (lda < 0) lda = D.n;
     constexpr int SPL = CtCfg<RPL, NS>::SPL;
     const int m = D.m, n = D.n, nvc = D.nvc;
     unsigned negm[RPL];
@@ -496,16 +503,31 @@ __device__ __forceinline__ int ct_build(const CtDims &D, CtState<RPL, NS> &S, co
         negm[k] = __ballot_sync(kFull, neg);
         const double sgn = neg ? -1.0 : 1.0;
         S.rhs[k] = live ? __dmul_rn(bi, sgn) : 0.0;
-        const double *arow = Ag + (size_t)(live ? row : 0) * n;
+        const double *arow = Ag + (size_t)(live ? row : 0) * lda;
+        if constexpr (V2) {     // n even, 16-byte aligned rows (the TMA-staged copy)
 #pragma unroll
-        for (int c = 0; c < NS; ++c) {
-            double v = 0.0;
-            if (live && c < n) {
-                const double x = arow[c];
-                nonfinite |= !isfinite(x);
-                v = __dmul_rn(x, sgn);
+            for (int c = 0; c < NS; c += 2) {
+                double v0 = 0.0, v1 = 0.0;
+                if (live && c < n) {
+                    const double2 x = *reinterpret_cast<const double2 *>(arow + c);
+                    nonfinite |= !(isfinite(x.x) && isfinite(x.y));
+                    v0 = __dmul_rn(x.x, sgn);
+                    v1 = __dmul_rn(x.y, sgn);
+                }
+                S.a[k][c] = v0;
+                if (c + 1 < NS) S.a[k][c + 1] = v1;
             }
-            S.a[k][c] = v;
+        } else {
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                double v = 0.0;
+                if (live && c < n) {
+                    const double x = arow[c];
+                    nonfinite |= !isfinite(x);
+                    v = __dmul_rn(x, sgn);
+                }
+                S.a[k][c] = v;
+            }
         }
     }
     int n_art = 0;
@@ -643,15 +665,53 @@ condensed_kernel(Batch B) {
         for (int q = D.lane; q < NS; q += 32) rvec[q] = 0.0;   // unused slots read as 0
     }
     CtState<RPL, NS> S;
+    // TMA staging (the launch granted STG_END bytes): LP k+1's A is bulk-copied into shared
+    // memory (one cp.async.bulk per row, completion on an mbarrier) while LP k solves; the
+    // build then reads it with 128-bit shared loads instead of per-lane strided global rows.
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const bool stg = dyn >= C::STG_END && !B.shared_Ab && (n & 1) == 0 &&
+                     (reinterpret_cast<uintptr_t>(B.A) & 15) == 0 && m <= 32 * RPL && n <= NS;
+    const unsigned sbar = (unsigned)__cvta_generic_to_shared(smem + C::STG_BAR);
+    const unsigned sbuf = (unsigned)__cvta_generic_to_shared(smem + C::STG);
+    const int lda = n + 2;             // staged row stride (doubles)
+    unsigned sphase = 0;
+    auto stage = [&](long long q) {
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the build's reads before the overwrite
+        if (D.lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"((unsigned)(m * n * 8))
+                         : "memory");
+        __syncwarp();
+        const double *src = B.A + (size_t)q * m * n;
+        for (int r = D.lane; r < m; r += 32)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(sbuf + (unsigned)(r * lda * 8)), "l"(src + (size_t)r * n), "r"((unsigned)(n * 8)), "r"(sbar)
+                         : "memory");
+    };
     long long lp = 0;
     if (D.lane == 0) lp = atomicAdd(B.next_lp, 1);
     lp = __shfl_sync(kFull, lp, 0);
+    if (stg) {
+        if (D.lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (lp < B.count) stage(lp);
+    }
     for (;;) {
         if (lp >= B.count) break;
         long long nxt = 0;                 // claim the next LP and warm L2 with its inputs
         if (D.lane == 0) nxt = atomicAdd(B.next_lp, 1);
         nxt = __shfl_sync(kFull, nxt, 0);
-        if (nxt < B.count) prefetch_lp_inputs(B, nxt, D.lane);
+        if (nxt < B.count) {
+            if (!stg) prefetch_lp_inputs(B, nxt, D.lane);
+            else if (D.lane == 0) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(B.b + (size_t)nxt * m));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(B.c + (size_t)nxt * n));
+            }
+        }
         const double *Ag = B.shared_Ab ? B.A : B.A + (size_t)lp * m * n;
         const double *bg = B.shared_Ab ? B.b : B.b + (size_t)lp * m;
         const double *cg = B.c + (size_t)lp * n;
@@ -683,7 +743,20 @@ condensed_kernel(Batch B) {
             }
         } else {
             bool nonfinite = false;
-            const int n_art = ct_build<RPL, NS>(D, S, Ag, bg, cg, nonfinite);
+            int n_art;
+            if (stg) {
+                unsigned done;
+                do {
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(sbar), "r"(sphase) : "memory");
+                } while (!done);
+                sphase ^= 1u;
+                n_art = ct_build<RPL, NS, true>(D, S, reinterpret_cast<const double *>(smem + C::STG), bg, cg, nonfinite,
+                                                lda);
+                if (nxt < B.count) stage(nxt);   // overlaps this LP's solve
+            } else {
+                n_art = ct_build<RPL, NS>(D, S, Ag, bg, cg, nonfinite);
+            }
             if (__any_sync(kFull, nonfinite)) {
                 status = kInvalid;
                 done = true;

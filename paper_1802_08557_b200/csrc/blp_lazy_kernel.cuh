@@ -94,9 +94,11 @@ __host__ __device__ inline long long lazy_scratch_doubles(int m, int n) {
 // Initial tableau cell a^0_ij of a single-phase LP (all row signs +1):
 // [A | I] (tableau.py:149-170).
 // Load-path knobs, measured (C5 / C4 / random 100x100): plain loads 5.74 / 65.0 / 0.83 ms;
-// __ldcg history 6.39 / 73.2 / 0.95; __ldg for A no change.
+// __ldcg history 6.39 / 73.2 / 0.95; __ldg for A no change.  Round 2 (C5 1e4 / random
+// 100 x 100 2e4, two alternating runs each): history loads and stores with an L2 evict_last
+// policy (mode 2) 5.34-5.35 / 0.860-0.861 ms vs plain 5.396-5.397 / 0.885-0.889 -- the default.
 #ifndef LAZY_HIST_MODE
-#define LAZY_HIST_MODE 0
+#define LAZY_HIST_MODE 2
 #endif
 #ifndef LAZY_A_MODE
 #define LAZY_A_MODE 0
@@ -108,12 +110,29 @@ __device__ __forceinline__ double lazy_a0(const double *Ag, int n, int i, int j)
     return j < n ? Ag[(size_t)i * n + j] : ((j - n == i) ? 1.0 : 0.0);
 #endif
 }
-// A replay-history load (written earlier by this CTA)
+// A replay-history load (written earlier by this CTA).  LAZY_HIST_MODE 2: history loads and
+// stores carry an L2 evict_last policy (the validation stream is evict-first).
+__device__ __forceinline__ unsigned long long lazy_pol() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ double lazy_h(const double *p) {
 #if LAZY_HIST_MODE == 1
     return __ldcg(p);
+#elif LAZY_HIST_MODE == 2
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(lazy_pol()));
+    return v;
 #else
     return *p;
+#endif
+}
+__device__ __forceinline__ void lazy_hs(double *p, double v) {
+#if LAZY_HIST_MODE == 2
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(lazy_pol()) : "memory");
+#else
+    *p = v;
 #endif
 }
 
@@ -178,7 +197,9 @@ __device__ __forceinline__ void lazy_bulk_load(unsigned dst, const void *src, un
 
 // FS = 1: the first KF pivots' f^t vectors live in shared memory after the
 // layout (KF from the launch's dynamic shared-memory size), later ones in the
-// L2 scratch.
+// L2 scratch.  FS = 2: their r^t vectors too (f^t then r^t per pivot) -- every
+// later pivot replays the whole r history of the pivot row, so the first
+// pivots' rows are the most re-read bytes of the kernel.
 template <int NT, int MINB, int WS, int RP, int FS = 0>
 __global__ void __launch_bounds__(NT, MINB)
 lazy_kernel(Batch B) {
@@ -197,6 +218,7 @@ lazy_kernel(Batch B) {
     constexpr int PT = WS ? NT - 32 * kLazyScanWarps : NT;    // pivot threads
     constexpr int NW = PT / 32;
     static_assert(!WS || PT >= 64, "WS needs pivot warps");
+    static_assert(FS == 0 || RP == 0, "shared-memory history only with the direct replay");
     int *s_res = reinterpret_cast<int *>(smem + L.off_misc + 8);             // status, iterations, deferred
     unsigned long long *fullb = reinterpret_cast<unsigned long long *>(smem + L.off_misc + 32);
     const unsigned ring = (unsigned)__cvta_generic_to_shared(smem + lazy_ring_offset(L, NT, RP));
@@ -218,18 +240,24 @@ lazy_kernel(Batch B) {
     const size_t HS = (size_t)gridDim.x * (size_t)(m + nv);     // pivot t -> t+1, same CTA
     double *Fh = B.gtab + (size_t)blockIdx.x * (size_t)(m + nv);
     double *Rh = Fh + m;
-    double *Fs = nullptr;
+    double *Fs = nullptr, *Rs = nullptr;
     int KF = 0;
     if constexpr (FS) {
         unsigned dyn;
         asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
         const size_t base = (lazy_smem_bytes(m, n, WS, NT, RP) + 15) / 16 * 16;
+        const size_t per = 8 * (size_t)(m > 0 ? m : 1) + (FS == 2 ? 8 * (size_t)nv : 0);
+        KF = (int)min((size_t)kLazyMaxPivots, (dyn - base) / per);
         Fs = reinterpret_cast<double *>(smem + base);
-        KF = (int)min((size_t)kLazyMaxPivots, (dyn - base) / (8 * (size_t)(m > 0 ? m : 1)));
+        Rs = Fs + (size_t)KF * m;                   // FS == 2: r^t of pivot t at Rs + t * nv
     }
     auto Fget = [&](int t, int i) -> double {
         if constexpr (FS) { if (t < KF) return Fs[(size_t)t * m + i]; }
         return lazy_h(Fh + (size_t)t * HS + i);
+    };
+    auto Rget = [&](int t, int j) -> double {
+        if constexpr (FS == 2) { if (t < KF) return Rs[(size_t)t * nv + j]; }
+        return lazy_h(Rh + (size_t)t * HS + j);
     };
     const int max_iter = B.lim.max_iterations > 0 ? B.lim.max_iterations : 50 * (m + n);
     const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
@@ -440,13 +468,13 @@ lazy_kernel(Batch B) {
                         a = t0 ? hw[t0 - 1] : lazy_a0(Ag, n, i, e);
                         a = lazy_replay(a, Fh + i, (int)HS, hw, t0, k);
                     } else {
-                        a = t0 ? lazy_h(Rh + (size_t)(t0 - 1) * HS + e) : lazy_a0(Ag, n, i, e);
+                        a = t0 ? Rget(t0 - 1, e) : lazy_a0(Ag, n, i, e);
                         for (int t = t0; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), lazy_h(Rh + (size_t)t * HS + e)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), Rget(t, e)));
                     }
                     fcur[i] = a;
                     if (FS && k < KF) Fs[(size_t)k * m + i] = a;
-                    else Fh[(size_t)k * HS + i] = a;
+                    else lazy_hs(Fh + (size_t)k * HS + i, a);
                     const unsigned long long key = key_min(ratio_entry(rhs[i], a));
                     if (key < lk) { lk = key; li = i; }     // rows ascend per thread
                 }
@@ -479,22 +507,23 @@ lazy_kernel(Batch B) {
                 // pivot row by replay, divided by pe; objective row; next candidates
                 unsigned long long ck = kKeyEmptyMax;
                 int ci = kNone, cb = kNone;
-                double *Rk = Rh + (size_t)k * HS;
+                double *Rk = (FS == 2 && k < KF) ? Rs + (size_t)k * nv : Rh + (size_t)k * HS;
                 if constexpr (RP == 1) {
                     __syncwarp();
                     for (int t = t0l + lane; t < k; t += 32) hw[t] = Fget(t, l);   // f^t_l
                     __syncwarp();
                 }
                 for (int j = tid; j < nv; j += PT) {
-                    double a = t0l ? lazy_h(Rh + (size_t)(t0l - 1) * HS + j) : lazy_a0(Ag, n, l, j);
+                    double a = t0l ? Rget(t0l - 1, j) : lazy_a0(Ag, n, l, j);
                     if constexpr (RP == 1) {
                         a = lazy_replay(a, Rh + j, (int)HS, hw, t0l, k);
                     } else {
                         for (int t = t0l; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), lazy_h(Rh + (size_t)t * HS + j)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), Rget(t, j)));
                     }
                     const double r = div_entry(a, pe);
-                    Rk[j] = r;
+                    if (FS == 2 && k < KF) Rk[j] = r;
+                    else lazy_hs(Rk + j, r);
                     const double v = __dsub_rn(rc[j], __dmul_rn(rce, r));
                     rc[j] = v;
                     if (!((j == e) || (j != oldvar && isb[j]))) {

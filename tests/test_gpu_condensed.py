@@ -166,3 +166,54 @@ def test_condensed_non_finite_flags(condensed):
     got = _native.solve_host(A, b, c, _native.make_limits())
     assert (got["status"][[3, 5, 9]] == 5).all()
     assert (np.delete(got["status"], [3, 5, 9]) != 5).all()
+
+
+STAGE_SHAPES = [(1, 2), (5, 6), (12, 19), (28, 32), (30, 31), (32, 32), (20, 40), (31, 64), (40, 16), (64, 32),
+                (100, 16)]
+
+
+@pytest.mark.parametrize("stage", ["0", "2"])
+@pytest.mark.parametrize("m,n", STAGE_SHAPES)
+def test_condensed_tma_staging(m, n, stage, condensed, monkeypatch):
+    """The one-warp kernel with its TMA staging of the next LP's A (BLP_CT_STAGE=2: one
+    cp.async.bulk per row into shared memory, mbarrier completion) and without it (0): the
+    same results as the oracle; odd n (rows not 16-byte multiples) falls back in-kernel."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import _native, batch_solve_arrays
+    monkeypatch.setenv("BLP_CMULTI", "0")
+    monkeypatch.setenv("BLP_CT_STAGE", stage)
+    variant = _native.kernel_variant(m, n)
+    assert variant.startswith("ctab"), variant
+    A, b, c = _mix(m, n, seed=m * 997 + n, count=160)
+    want = oracle.solve_batch(A, b, c)
+    compare(_d(batch_solve_arrays(A, b, c)), want, f"{variant} {m}x{n} stage={stage}")
+    A[7, m - 1, n - 1] = np.nan      # validation is fused into the (staged) build
+    got = _native.solve_host(A, b, c, _native.make_limits())
+    assert got["status"][7] == 5
+    assert np.array_equal(np.delete(got["status"], 7), np.delete(want["status"], 7))
+
+
+def test_condensed_tma_staging_unaligned_device_pointer(condensed, monkeypatch):
+    """A caller's device A that is only 8-byte aligned (a view one double into a buffer):
+    the kernel must not issue bulk copies from it (16-byte alignment) and still match."""
+    from oracle import oracle
+    from paper_1802_08557_b200 import SolverLimits, _native, workloads
+    monkeypatch.setenv("BLP_CT_STAGE", "2")
+    A, b, c = workloads.afiro_arrays(300, seed=5, m=28, n=32)
+    want = oracle.solve_batch(A, b, c)
+    dev = torch.device("cuda:0")
+    buf = torch.zeros(A.size + 1, dtype=torch.float64, device=dev)
+    buf[1:] = torch.from_numpy(A.reshape(-1)).to(dev)
+    tA = buf[1:].view(A.shape)
+    assert tA.data_ptr() % 16 == 8
+    tb, tc = (torch.from_numpy(np.ascontiguousarray(v)).to(dev) for v in (b, c))
+    cnt, nn = c.shape
+    out = dict(status=torch.empty(cnt, dtype=torch.int8, device=dev),
+               objective=torch.empty(cnt, dtype=torch.float64, device=dev),
+               x=torch.empty(cnt, nn, dtype=torch.float64, device=dev),
+               it1=torch.empty(cnt, dtype=torch.int32, device=dev),
+               it2=torch.empty(cnt, dtype=torch.int32, device=dev))
+    _native.solve_device(tA, tb, tc, SolverLimits().to_native(), out)
+    torch.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    compare(got, want, "ctab 28x32 unaligned A")
