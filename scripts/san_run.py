@@ -25,7 +25,7 @@ CASES = {
     "quadlp_c3": ("c3:8", {"BLP_LAZY_SMALL": "0", "BLP_CMULTI": "0"}),
     "cmulti_c3": ("c3:8", {"BLP_LAZY_SMALL": "0"}),
     "cmulti_lazy_c3": ("c3:8", {}),
-    "cmulti_c4": ("afiro:64:32:24", {"BLP_CMULTI": "2", "BLP_LAZY_SMALL": "0"}),
+    "cmulti_c4": ("afiro:64:32:24", {"BLP_CMULTI": "3", "BLP_LAZY_SMALL": "0"}),
     "condensed_p1": ("support2:64", {}),
     "lazy_c3": ("random:100:12", {}),
     "lazy_support": ("support:64", {"BLP_CONDENSED": "0"}),

@@ -68,18 +68,18 @@ SHAPES = [(1, 1), (2, 3), (5, 5), (8, 8), (12, 19), (28, 32), (30, 31), (32, 32)
           (33, 20), (40, 16), (64, 32), (64, 8), (50, 30), (65, 8), (100, 16), (128, 16), (90, 7)]
 
 
-@pytest.mark.parametrize("cm", ["0", "2"])
+@pytest.mark.parametrize("cm", ["0", "3"])
 @pytest.mark.parametrize("m,n", SHAPES)
 def test_condensed_matches_oracle(m, n, cm, condensed, monkeypatch):
     """Every shape through the one-warp form (BLP_CMULTI=0) and, for 33..128 rows, the
-    multi-warp form (BLP_CMULTI=2, blp_cmulti_kernel.cuh) too."""
+    multi-warp form (BLP_CMULTI=3, blp_cmulti_kernel.cuh) too."""
     from oracle import oracle
     from paper_1802_08557_b200 import _native, batch_solve_arrays
     monkeypatch.setenv("BLP_CMULTI", cm)
-    if cm == "2" and m <= 32:
+    if cm == "3" and m <= 32:
         pytest.skip("the multi-warp form starts at 33 rows")
     variant = _native.kernel_variant(m, n)
-    assert variant.startswith("cm" if cm == "2" else "ctab"), variant
+    assert variant.startswith("cm" if cm == "3" else "ctab"), variant
     A, b, c = _mix(m, n, seed=m * 1000 + n)
     want = oracle.solve_batch(A, b, c)
     compare(_d(batch_solve_arrays(A, b, c)), want, f"{variant} {m}x{n}")

@@ -226,7 +226,7 @@ def test_every_kernel_family_matches_oracle(m, n, monkeypatch):
     A, b, c = (np.concatenate(v) for v in ((A1, A2), (b1, b2), (c1, c2)))
     want = oracle.solve_batch(A, b, c)
     seen = set()
-    for force, hbm, cm in (("", "0", "1"), ("condensed", "0", "0"), ("condensed", "0", "2"), ("warplp", "0", "1"),
+    for force, hbm, cm in (("", "0", "1"), ("condensed", "0", "0"), ("condensed", "0", "3"), ("warplp", "0", "1"),
                            ("pairlp", "0", "1"), ("regtile", "0", "1"), ("smem", "0", "1"), ("smem", "1", "1")):
         monkeypatch.setenv("BLP_KERNEL", force)
         monkeypatch.setenv("BLP_FORCE_HBM", hbm)

@@ -45,12 +45,12 @@ def test_c4b_directions_match_oracle():
     assert (got["it1"] == want["it1"][0]).all() and want["it1"][0] > 0
 
 
-@pytest.mark.parametrize("cm", ["0", "2"])
+@pytest.mark.parametrize("cm", ["0", "3"])
 @pytest.mark.parametrize("m,n", [(20, 12), (28, 32), (40, 16), (64, 8), (100, 12), (64, 32), (100, 100), (120, 128),
                                  (160, 48), (220, 150), (400, 60)])
 def test_shared_phase1_every_condensed_shape(m, n, cm, monkeypatch):
     """Every condensed instance family -- one warp (rows per lane 1/2/4; BLP_CMULTI=0) and
-    multi-warp (cmulti, registers + tile; BLP_CMULTI=2) -- with a mixed-sign shared b:
+    multi-warp (cmulti, registers + tile; BLP_CMULTI=3) -- with a mixed-sign shared b:
     afiro-recipe polytopes, feasible and infeasible, random directions."""
     from oracle import oracle
     from paper_1802_08557_b200 import _native, workloads
@@ -58,7 +58,7 @@ def test_shared_phase1_every_condensed_shape(m, n, cm, monkeypatch):
     variant = _native.kernel_variant(m, n, True)
     if not variant.startswith(("ctab", "cm")):
         pytest.skip(f"{m}x{n}: no one-warp instance")
-    assert variant.startswith("cm" if cm == "2" and m > 32 else "ctab"), variant
+    assert variant.startswith("cm" if cm == "3" and m > 32 else "ctab"), variant
     for seed in range(4):
         A, b, _ = workloads.afiro_arrays(1, seed=100 + seed, m=m, n=n, infeasible_frac=0.5)
         C = np.random.default_rng(seed).integers(-20, 51, size=(300, n)).astype(np.float64)
