@@ -81,12 +81,14 @@ bool select(int m, int n, Instance *out) {
     if (m < 1 || n < 1) return false;
     // BLP_CMULTI: 0 never, 1 for 65..128 rows and where the one-warp form has no instance,
     // 3 for every 33..128-row shape, 2 (default) as 3 except narrow LPs, which the one-warp
-    // form (2 or 4 rows per lane) solves faster.  Measured (afiro recipe, 1e5 LPs, one-warp vs
-    // multi-warp incl. its lazy pre-pass): 64 x 8 5.18 vs 8.93 ms, 128 x 8 16.0 vs 34.8,
-    // 64 x 16 10.9 vs 11.8, 100 x 16 36.3 vs 37.0, but 40 x 16 8.33 vs 8.06; C4 64 x 32
+    // form (2 or 4 rows per lane) solves faster.  Measured (1e5 LPs, one-warp vs multi-warp
+    // incl. its lazy pre-pass): afiro recipe (two-phase) 64 x 8 5.18 vs 8.93 ms, 128 x 8 16.0
+    // vs 34.8, 64 x 16 10.9 vs 11.8, 100 x 16 36.3 vs 37.0, but 40 x 16 8.33 vs 8.06; the
+    // reference's random LPs (single phase, few pivots) 64 x 8 0.40 vs 0.57, 64 x 16 0.69 vs
+    // 0.80, but 128 x 16 1.75 vs 1.42 (the one-warp form has no lazy pre-pass); C4 64 x 32
     // (1e6 directions) ctab_r2_s32 42.0 vs cm2_r16_s16 37.1 ms.
     const int cm = env_int("BLP_CMULTI", 2);
-    const bool narrow = n <= 8 || (n <= 16 && m > 48);
+    const bool narrow = n <= 8 || (n <= 16 && m > 48 && m <= 64);
     if (m > 32 && m <= 512 && cm != 0) {
         const int nwr = m <= 64 ? 2 : (m <= 128 ? 4 : (m <= 256 ? 8 : 16));
         const bool one_warp_fits = (m <= 64 && n <= 32) || (m > 64 && m <= 128 && n <= 16);
