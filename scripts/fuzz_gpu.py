@@ -23,7 +23,7 @@ from oracle import oracle  # noqa: E402
 from paper_1802_08557_b200 import _native, workloads  # noqa: E402
 
 FORCE = [{}, {}, {}, {"BLP_CMULTI": "0"}, {"BLP_CONDENSED": "0"}, {"BLP_LAZY_SMALL": "0"}, {"BLP_LAZY": "0"},
-         {"BLP_KERNEL": "smem"}, {"BLP_LAZY_SPLIT": "1"}]
+         {"BLP_KERNEL": "smem"}, {"BLP_LAZY_SPLIT": "1"}, {"BLP_CT_STAGE": "2"}, {"BLP_CMULTI": "3"}]
 
 
 def recipe(rng, m, n, cnt, seed):

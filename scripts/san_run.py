@@ -18,6 +18,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 # name: (generator, env knobs); generators are the workloads recipes at small counts
 CASES = {
     "condensed_c2": ("afiro:28:32:64", {}),
+    "condensed_c2_direct": ("afiro:28:32:64", {"BLP_CT_STAGE": "0"}),
+    "condensed_stage_short": ("afiro:20:10:64", {"BLP_CT_STAGE": "2"}),
+    "condensed_narrow": ("afiro:64:8:64", {}),
     "condensed_c4": ("support:64", {}),
     "warplp2_c2": ("afiro:28:32:64", {"BLP_CONDENSED": "0"}),
     "warplp_c1": ("random:5:64", {"BLP_CONDENSED": "0"}),

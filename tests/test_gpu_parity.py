@@ -302,7 +302,7 @@ def test_cluster_kernel_matches_oracle(shape, K, monkeypatch):
     compare(_native_dict(res), want, f"cluster {shape} K={K}")
 
 
-LAZY_CASES = [(150, 150), (300, 200), (100, 150), (40, 300)]   # 500 x 500: the c5 goldens
+LAZY_CASES = [(150, 150), (300, 200), (100, 150), (40, 300), (64, 30)]   # 500 x 500: the c5 goldens
 
 
 def _single_phase_mix(m, n, seed):
@@ -321,14 +321,17 @@ def _single_phase_mix(m, n, seed):
     return A, b, c
 
 
+@pytest.mark.parametrize("sparse", ["1", "0"])
 @pytest.mark.parametrize("m,n", LAZY_CASES)
-def test_lazy_tableau_matches_oracle(m, n, monkeypatch):
+def test_lazy_tableau_matches_oracle(m, n, sparse, monkeypatch):
     """The exact lazy-tableau kernel (entering column and pivot row evaluated by replaying
     the rank-1 update history) on single-phase LPs, with the cluster kernel taking the
     LPs it defers (phase 1 needed / more than 64 pivots): equal to the oracle, including
-    iteration limits hit inside the lazy kernel."""
+    iteration limits hit inside the lazy kernel.  BLP_LAZY_SPARSE=1 (default for m >= 64):
+    the slack columns of rows never pivoted on are skipped as exact unit columns."""
     from oracle import oracle
     from paper_1802_08557_b200 import SolverLimits, _native, batch_solve_arrays
+    monkeypatch.setenv("BLP_LAZY_SPARSE", sparse)
     A, b, c = _single_phase_mix(m, n, seed=m * 7 + n)
     monkeypatch.setenv("BLP_KERNEL", "cluster")
     assert _native.kernel_variant(m, n).startswith("lazy")
