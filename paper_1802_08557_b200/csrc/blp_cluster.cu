@@ -55,7 +55,19 @@ const char *variant_name(int m, int n) {
     return lazy_enabled(m, n) ? "lazy+cluster_r32" : "cluster_r32";
 }
 
-cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *clusters_used) {
+namespace {
+// A prepared cluster launch: the configuration (cluster size K from the occupancy calculator)
+// and its workspace, allocated and cleared on the stream (cluster_prepare) ahead of the
+// launch itself (cluster_fire), so that a programmatic dependent launch can follow the lazy
+// kernel directly.
+struct ClusterLaunch {
+    int K = 0;
+    long long clusters = 0;
+    size_t smem = 0;
+    void *ws = nullptr;
+};
+
+cudaError_t cluster_prepare(const blp::Batch &B, cudaStream_t stream, ClusterLaunch *CL) {
     KernelFn fn = kernel_fn();
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
@@ -88,45 +100,57 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
         if (nc * K > bestC * bestK) { bestK = K; bestC = nc; bestS = s; }
     }
     if (!bestK) return cudaErrorInvalidConfiguration;
-    long long clusters = std::min<long long>(bestC, B.count);
+    CL->K = bestK;
+    CL->clusters = std::min<long long>(bestC, B.count);
+    CL->smem = bestS;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bestS);
     if (e != cudaSuccess) return e;
     // workspace: the LP queue head + per cluster [2 parities][K CTAs][ld] published columns
     const blp::ClLayout L = blp::make_cl_layout(B.m, B.n, bestK, kRC);
-    const size_t scratch = (size_t)clusters * 2 * bestK * L.ld * sizeof(double);
-    void *ws = nullptr;
-    e = cudaMallocAsync(&ws, 256 + scratch, stream);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(ws, 0, 256, stream);
-    if (e != cudaSuccess) { cudaFreeAsync(ws, stream); return e; }
+    const size_t scratch = (size_t)CL->clusters * 2 * bestK * L.ld * sizeof(double);
+    e = cudaMallocAsync(&CL->ws, 256 + scratch, stream);
+    if (e != cudaSuccess) { CL->ws = nullptr; return e; }
+    e = cudaMemsetAsync(CL->ws, 0, 256, stream);
+    if (e != cudaSuccess) { cudaFreeAsync(CL->ws, stream); CL->ws = nullptr; }
+    return e;
+}
+
+// pdl: a programmatic dependent launch after the lazy kernel (which triggers its dependents
+// at its start): the cluster grid is scheduled onto SMs as the lazy kernel's CTAs retire and
+// waits in griddepcontrol.wait for its completion, so the launch of a dense pass that is
+// often empty (C5: no LP deferred) overlaps the lazy kernel's tail instead of following it.
+// Measured neutral (C5 1e4: 5.331 / 5.328 ms vs 5.332 / 5.330 with BLP_PDL=0; random 300 x
+// 300: 1.397 / 1.388 vs 1.397 / 1.392): the empty launch was already off the critical path.
+cudaError_t cluster_fire(const blp::Batch &B, const ClusterLaunch &CL, cudaStream_t stream, bool pdl) {
+    KernelFn fn = kernel_fn();
     blp::Batch Bl = B;
-    Bl.next_lp = reinterpret_cast<int *>(ws);
-    Bl.gtab = reinterpret_cast<double *>(reinterpret_cast<char *>(ws) + 256);
+    Bl.next_lp = reinterpret_cast<int *>(CL.ws);
+    Bl.gtab = reinterpret_cast<double *>(reinterpret_cast<char *>(CL.ws) + 256);
     Bl.gtab_stride = 0;
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = bestK;
+    attr[0].val.clusterDim.x = CL.K;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((unsigned)(clusters * bestK), 1, 1);
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)(CL.clusters * CL.K), 1, 1);
     cfg.blockDim = dim3(kNT, 1, 1);
-    cfg.dynamicSmemBytes = bestS;
+    cfg.dynamicSmemBytes = CL.smem;
     cfg.stream = stream;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     if (env_int("BLP_VERBOSE", 0))
-        fprintf(stderr, "blp cluster: m=%d n=%d K=%d clusters=%lld smem=%zu+%zu\n", B.m, B.n, bestK, clusters, bestS,
-                sizeof(blp::ClStatic<kRC>));
-    if (K_used) *K_used = bestK;
-    if (clusters_used) *clusters_used = (int)clusters;
+        fprintf(stderr, "blp cluster: m=%d n=%d K=%d clusters=%lld smem=%zu+%zu pdl=%d\n", B.m, B.n, CL.K, CL.clusters,
+                CL.smem, sizeof(blp::ClStatic<kRC>), pdl ? 1 : 0);
 #ifdef BLP_CL_PROF
     {
         unsigned long long z[16] = {};
         cudaMemcpyToSymbolAsync(blp::g_cl_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, stream);
     }
 #endif
-    e = cudaLaunchKernelEx(&cfg, fn, Bl);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, Bl);
 #ifdef BLP_CL_PROF
     {
         unsigned long long h[16];
@@ -141,8 +165,20 @@ cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *c
         fprintf(stderr, "  total Gcyc=%.3f\n", tot / 1e9);
     }
 #endif
-    const cudaError_t ef = cudaFreeAsync(ws, stream);
+    const cudaError_t ef = cudaFreeAsync(CL.ws, stream);
     return e != cudaSuccess ? e : ef;
+}
+
+
+}  // namespace
+
+cudaError_t launch(const blp::Batch &B, cudaStream_t stream, int *K_used, int *clusters_used) {
+    ClusterLaunch CL;
+    const cudaError_t e = cluster_prepare(B, stream, &CL);
+    if (e != cudaSuccess) return e;
+    if (K_used) *K_used = CL.K;
+    if (clusters_used) *clusters_used = (int)CL.clusters;
+    return cluster_fire(B, CL, stream, false);
 }
 
 static int lazy_ws_mode(const blp::Batch &B, int nt) {
@@ -189,6 +225,14 @@ cudaError_t launch_lazy(const blp::Batch &B, cudaStream_t stream, int **defer_li
            : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16, 0, 1>
            : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32, 0, 1>
                        : (LazyFn)blp::lazy_kernel<256, 4, 0, 1>;
+    else if (B.m >= blp::kLazyMaxPivots && env_int("BLP_LAZY_SPARSE", 0))
+        // BLP_LAZY_SPARSE=1: slack columns of rows never pivoted on are exact unit columns,
+        // skipped (SPX; measured slower: C5 5.61 vs 5.34 ms -- blp_lazy_kernel.cuh)
+        fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2, 0, 0, 0, 1>
+           : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8, 0, 0, 0, 1>
+           : nt == 64  ? (LazyFn)blp::lazy_kernel<64, 16, 0, 0, 0, 1>
+           : nt == 32  ? (LazyFn)blp::lazy_kernel<32, 32, 0, 0, 0, 1>
+                       : (LazyFn)blp::lazy_kernel<256, 4, 0, 0, 0, 1>;
     else
         fn = nt == 512 ? (LazyFn)blp::lazy_kernel<512, 2, 0, 0>
            : nt == 128 ? (LazyFn)blp::lazy_kernel<128, 8, 0, 0>
@@ -341,12 +385,24 @@ cudaError_t finish_lazy(const blp::Batch &B, cudaStream_t stream, void *ws) {
 cudaError_t launch_lazy_then_cluster(const blp::Batch &B, cudaStream_t stream) {
     int *dl = nullptr, *dc = nullptr;
     void *ws = nullptr;
-    cudaError_t e = launch_lazy(B, stream, &dl, &dc, &ws);
+    // the dense pass is prepared (workspace cleared) before the lazy kernel so that it can
+    // follow it as a programmatic dependent launch (BLP_PDL=0: a plain stream-ordered launch;
+    // support mode clears its flags after the lazy kernel, so it launches plainly)
+    ClusterLaunch CL;
+    cudaError_t e = cluster_prepare(B, stream, &CL);
+    if (e == cudaSuccess) e = launch_lazy(B, stream, &dl, &dc, &ws);
     if (e == cudaSuccess) {
         blp::Batch Bc = B;                       // the dense kernel solves the deferred LPs
         Bc.defer_list = dl;
         Bc.defer_count = dc;
-        e = launch(Bc, stream, nullptr, nullptr);
+        const bool pdl = !B.shared_Ab && env_int("BLP_PDL", 1) != 0;
+#ifndef BLP_AB_NODENSE   // A/B builds only: the cost of the (possibly empty) dense launch
+        e = cluster_fire(Bc, CL, stream, pdl);
+#else
+        cudaFreeAsync(CL.ws, stream);
+#endif
+    } else if (CL.ws) {
+        cudaFreeAsync(CL.ws, stream);
     }
     const cudaError_t ef = finish_lazy(B, stream, ws);
     return e != cudaSuccess ? e : ef;

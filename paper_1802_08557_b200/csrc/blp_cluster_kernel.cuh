@@ -611,6 +611,10 @@ template <int RC, int NT>
 __global__ void __launch_bounds__(NT, 1)
 cluster_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
+    // launched as a programmatic dependent of the lazy kernel (blp_cluster.cu cluster_fire):
+    // nothing it reads (the deferral list, the LP queue) is valid before that grid completes;
+    // a no-op for a plain launch
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     ClStatic<RC> &S = cl_static<RC>();
     const int m = B.m, n = B.n, nv = n + m;
     ClCtx X;

@@ -65,7 +65,7 @@ struct LazyPart {
 };
 
 struct LazyLayout {
-    size_t off_rhs, off_rc, off_fcur, off_basis, off_last, off_isb, off_part, off_misc;
+    size_t off_rhs, off_rc, off_fcur, off_basis, off_last, off_isb, off_part, off_misc, off_first, off_urow;
     size_t bytes;
 };
 
@@ -82,6 +82,8 @@ __host__ __device__ inline LazyLayout make_lazy_layout(int m, int n) {
     L.off_isb = o;   o = al(o + (size_t)nv);
     L.off_part = o;  o = al(o + sizeof(LazyPart));
     L.off_misc = o;  o = al(o + 64);
+    L.off_first = o; o = al(o + (size_t)mm * 4);
+    L.off_urow = o;  o = al(o + (size_t)kLazyMaxPivots * 4);
     L.bytes = o;
     return L;
 }
@@ -200,10 +202,24 @@ __device__ __forceinline__ void lazy_bulk_load(unsigned dst, const void *src, un
 // L2 scratch.  FS = 2: their r^t vectors too (f^t then r^t per pivot) -- every
 // later pivot replays the whole r history of the pivot row, so the first
 // pivots' rows are the most re-read bytes of the kernel.
-template <int NT, int MINB, int WS, int RP, int FS = 0>
+// SPX = 1 (m >= kLazyMaxPivots, direct replay): the slack block of the tableau is
+// E_k..E_1 I, which differs from I only in the columns of rows that have been pivot rows,
+// so the slack column of a row never pivoted on is exactly e_i (its pivot-row entries r^t
+// are exactly +0: 0 / pe with pe > 0, replayed as a - f * (+0) = a).  Those columns are
+// neither evaluated nor stored: the pivot row covers the n structural columns plus the
+// slack columns of rows already pivoted on, and r^t keeps a slack entry per first-pivot
+// slot u (row urow[u]) at offset n + u -- half the row replay and a third less history for C5.
+// Measured slower and kept opt-in (BLP_LAZY_SPARSE=1; parity-tested): C5 1e4 5.61 vs 5.34 ms,
+// random 100 x 100 (2e4) 0.918 vs 0.870, random 300 x 300 1.416 vs 1.385 -- a pivot is
+// latency-bound, the 512 threads still need two column rounds (n + k > 512 for C5), and the
+// skipped history loads were L2 hits.
+template <int NT, int MINB, int WS, int RP, int FS = 0, int SPX = 0>
 __global__ void __launch_bounds__(NT, MINB)
 lazy_kernel(Batch B) {
     extern __shared__ __align__(16) unsigned char smem[];
+    // the dense pass that follows may be a programmatic dependent launch: let it be scheduled
+    // now (it waits in griddepcontrol.wait for this grid to complete)
+    asm volatile("griddepcontrol.launch_dependents;");
     const int m = B.m, n = B.n, nv = n + m;
     const LazyLayout L = make_lazy_layout(m, n);
     double *rhs = reinterpret_cast<double *>(smem + L.off_rhs);
@@ -219,6 +235,9 @@ lazy_kernel(Batch B) {
     constexpr int NW = PT / 32;
     static_assert(!WS || PT >= 64, "WS needs pivot warps");
     static_assert(FS == 0 || RP == 0, "shared-memory history only with the direct replay");
+    static_assert(SPX == 0 || RP == 0, "sparse slack history only with the direct replay");
+    int *firstp = reinterpret_cast<int *>(smem + L.off_first);    // row -> first pivot slot, -1
+    int *urow = reinterpret_cast<int *>(smem + L.off_urow);       // slot u -> row first pivoted there, -1
     int *s_res = reinterpret_cast<int *>(smem + L.off_misc + 8);             // status, iterations, deferred
     unsigned long long *fullb = reinterpret_cast<unsigned long long *>(smem + L.off_misc + 32);
     const unsigned ring = (unsigned)__cvta_generic_to_shared(smem + lazy_ring_offset(L, NT, RP));
@@ -258,6 +277,11 @@ lazy_kernel(Batch B) {
     auto Rget = [&](int t, int j) -> double {
         if constexpr (FS == 2) { if (t < KF) return Rs[(size_t)t * nv + j]; }
         return lazy_h(Rh + (size_t)t * HS + j);
+    };
+    // SPX: r^t of column j (slack column n + i: u = row i's first pivot slot, -1 if none)
+    auto RgetS = [&](int t, int j, int u) -> double {
+        if (SPX && j >= n) return (u >= 0 && u <= t) ? Rget(t, n + u) : 0.0;
+        return Rget(t, j);
     };
     const int max_iter = B.lim.max_iterations > 0 ? B.lim.max_iterations : 50 * (m + n);
     const int trigger = B.lim.degenerate_limit >= 0 ? B.lim.degenerate_limit : (m > 1 ? m : 1);
@@ -330,6 +354,7 @@ lazy_kernel(Batch B) {
             rhs[i] = bi;                      // b * (+1)
             basis[i] = n + i;
             lastpiv[i] = 0;
+            if (SPX) firstp[i] = -1;
         }
         if (__syncthreads_or(neg)) {
             if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
@@ -431,12 +456,19 @@ lazy_kernel(Batch B) {
             int degenerate_run = 0;
             bool use_bland = false;
             int prev_l = -1, prev_e = -1, prev_old = -1;
+            bool prev_new = false;                    // SPX: prev_l was pivoted on for the first time
             double prev_rr = 0.0;
             // _run_phase (simplex.py:63-91)
             for (int k = 0;; ++k) {                   // pivot number k+1; history slot k
                 // previous pivot's bookkeeping (after the barrier that ended it)
                 if (prev_l >= 0) {
-                    if (tid == 0) { basis[prev_l] = prev_e; isb[prev_old] = 0; isb[prev_e] = 1; }
+                    if (tid == 0) {
+                        basis[prev_l] = prev_e; isb[prev_old] = 0; isb[prev_e] = 1;
+                        if (SPX) {
+                            urow[k - 1] = prev_new ? prev_l : -1;
+                            if (prev_new) firstp[prev_l] = k - 1;
+                        }
+                    }
                     if (tid == (prev_l % PT)) { lastpiv[prev_l] = k; rhs[prev_l] = prev_rr; }
                 }
                 if (k == max_iter) { status = kIterationLimit; iters = max_iter; break; }
@@ -461,6 +493,10 @@ lazy_kernel(Batch B) {
                     for (int t = lane; t < k; t += 32) hw[t] = lazy_h(Rh + (size_t)t * HS + e);   // r^t_e
                     __syncwarp();
                 }
+                // SPX: the entering slack's first-pivot slot (prev_l's entry is written by tid 0
+                // at the top of this pivot, so it comes from the registers)
+                int ue = -1;
+                if (SPX && e >= n) ue = (e - n == prev_l && prev_new) ? k - 1 : firstp[e - n];
                 for (int i = tid; i < m; i += PT) {
                     const int t0 = lastpiv[i];
                     double a;
@@ -468,9 +504,9 @@ lazy_kernel(Batch B) {
                         a = t0 ? hw[t0 - 1] : lazy_a0(Ag, n, i, e);
                         a = lazy_replay(a, Fh + i, (int)HS, hw, t0, k);
                     } else {
-                        a = t0 ? Rget(t0 - 1, e) : lazy_a0(Ag, n, i, e);
+                        a = t0 ? RgetS(t0 - 1, e, ue) : lazy_a0(Ag, n, i, e);
                         for (int t = t0; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), Rget(t, e)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, i), RgetS(t, e, ue)));
                     }
                     fcur[i] = a;
                     if (FS && k < KF) Fs[(size_t)k * m + i] = a;
@@ -513,17 +549,29 @@ lazy_kernel(Batch B) {
                     for (int t = t0l + lane; t < k; t += 32) hw[t] = Fget(t, l);   // f^t_l
                     __syncwarp();
                 }
-                for (int j = tid; j < nv; j += PT) {
-                    double a = t0l ? Rget(t0l - 1, j) : lazy_a0(Ag, n, l, j);
+                // SPX: structural columns, then the slack columns of rows pivoted on so far (slot u:
+                // row urow[u]; slot k is this pivot's row if it is new), stored at n + u
+                const int fl = SPX ? firstp[l] : 0;
+                const bool lnew = SPX && fl < 0;
+                const int jend = SPX ? n + k + 1 : nv;
+                for (int jj = tid; jj < jend; jj += PT) {
+                    int j = jj, u = -1;
+                    if (SPX && jj >= n) {
+                        u = jj - n;
+                        const int row = u == k ? (lnew ? l : -1) : urow[u];
+                        if (row < 0) continue;
+                        j = n + row;
+                    }
+                    double a = t0l ? RgetS(t0l - 1, j, u) : lazy_a0(Ag, n, l, j);
                     if constexpr (RP == 1) {
                         a = lazy_replay(a, Rh + j, (int)HS, hw, t0l, k);
                     } else {
                         for (int t = t0l; t < k; ++t)
-                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), Rget(t, j)));
+                            a = __dsub_rn(a, __dmul_rn(Fget(t, l), RgetS(t, j, u)));
                     }
                     const double r = div_entry(a, pe);
-                    if (FS == 2 && k < KF) Rk[j] = r;
-                    else lazy_hs(Rk + j, r);
+                    if (FS == 2 && k < KF) Rk[jj] = r;
+                    else lazy_hs(Rk + jj, r);
                     const double v = __dsub_rn(rc[j], __dmul_rn(rce, r));
                     rc[j] = v;
                     if (!((j == e) || (j != oldvar && isb[j]))) {
@@ -542,7 +590,7 @@ lazy_kernel(Batch B) {
                 for (int i = tid; i < m; i += PT)
                     if (i != l) rhs[i] = __dsub_rn(rhs[i], __dmul_rn(fcur[i], rrhs));
                 obj = __dadd_rn(obj, __dmul_rn(rce, rrhs));          // tableau.py:242
-                prev_l = l; prev_e = e; prev_old = oldvar; prev_rr = rrhs;
+                prev_l = l; prev_e = e; prev_old = oldvar; prev_rr = rrhs; prev_new = lnew;
                 pbar();  // S3
             }
             pbar();

@@ -327,8 +327,8 @@ def test_lazy_tableau_matches_oracle(m, n, sparse, monkeypatch):
     """The exact lazy-tableau kernel (entering column and pivot row evaluated by replaying
     the rank-1 update history) on single-phase LPs, with the cluster kernel taking the
     LPs it defers (phase 1 needed / more than 64 pivots): equal to the oracle, including
-    iteration limits hit inside the lazy kernel.  BLP_LAZY_SPARSE=1 (default for m >= 64):
-    the slack columns of rows never pivoted on are skipped as exact unit columns."""
+    iteration limits hit inside the lazy kernel.  BLP_LAZY_SPARSE=1 (opt-in, m >= 64): the
+    slack columns of rows never pivoted on are skipped as exact unit columns."""
     from oracle import oracle
     from paper_1802_08557_b200 import SolverLimits, _native, batch_solve_arrays
     monkeypatch.setenv("BLP_LAZY_SPARSE", sparse)
