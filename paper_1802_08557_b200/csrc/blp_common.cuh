@@ -72,6 +72,7 @@ struct Batch {
     int *vq;
     unsigned char *vflag;
     int vfirst;            // CTAs that take validation chunks before LPs (the rest: LPs first)
+    int lazy_discard = 0;  // lazy kernel: discard a solved LP's replay history from L2
 };
 
 // Number of LPs a kernel launch processes, and the batch index of its k-th.

@@ -400,6 +400,23 @@ lazy_kernel(Batch B) {
         int iters = 0;
         double obj = 0.0;
         bool deferred = false;
+        int hrows = 0;
+        // The LP's replay history is dead once it is solved: its L2 lines are discarded
+        // (discard.global.L2: no write-back of the dirty lines, the capacity freed for the
+        // live history of the other CTAs).  Only whole 128-byte lines inside this CTA's rows
+        // (the neighbouring CTAs' rows share the boundary lines).  BLP_LAZY_DISCARD=0 (launch
+        // sets B.lazy_discard) keeps them.
+        auto discard_history = [&]() {
+            if constexpr (WS) return;
+            if (!B.lazy_discard) return;
+            const size_t rowb = (size_t)(m + nv) * 8;
+            for (int t = 0; t < hrows; ++t) {
+                const uintptr_t base = reinterpret_cast<uintptr_t>(Fh + (size_t)t * HS);
+                const uintptr_t lo = (base + 127) & ~(uintptr_t)127, hi = (base + rowb) & ~(uintptr_t)127;
+                for (uintptr_t a = lo + (uintptr_t)tid * 128; a < hi; a += (uintptr_t)NT * 128)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+            }
+        };
         if (WS && tid >= PT) {
             // scanner warps: A through the bulk-copy ring while the pivot warps solve
             const int stid = tid - PT;
@@ -485,6 +502,7 @@ lazy_kernel(Batch B) {
                 }
                 if (e < 0) { iters = k; break; }   // optimal
                 if (k == kLazyMaxPivots) { deferred = true; break; }
+                hrows = k + 1;                       // history rows 0..k may hold this LP's data
                 const double rce = rc[e];
                 // entering column by replay (f_i = a_ie before this pivot); ratio test
                 unsigned long long lk = kKeyEmptyMin;
@@ -610,6 +628,7 @@ lazy_kernel(Batch B) {
         if (deferred) {
             if (tid == 0) B.defer_list[atomicAdd(B.defer_count, 1)] = (int)lp;
             __syncthreads();
+            discard_history();
             continue;
         }
         // ---- _extract_point (simplex.py:146-151) and c @ x ----
@@ -647,6 +666,7 @@ lazy_kernel(Batch B) {
             }
         }
         __syncthreads();
+        discard_history();
     }
 }
 
