@@ -23,6 +23,8 @@ p.add_argument("--steps", type=int, default=5)
 p.add_argument("--env", nargs="*", default=[""])
 p.add_argument("--max-iter", type=int, default=None, help="SolverLimits.max_iterations (per phase): isolates build cost")
 p.add_argument("--shape", default=None, help="recipe:m:n instead of a config (afiro | degenerate | random)")
+p.add_argument("--pipelined", action="store_true",
+               help="time the steps back to back in one event region (host work overlaps, as in bench.py)")
 a = p.parse_args()
 if a.shape:
     from paper_1802_08557_b200 import workloads
@@ -58,7 +60,15 @@ for setting in a.env:
     _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared)
     torch.cuda.synchronize()
     ts = []
-    for _ in range(a.steps):
+    if a.pipelined:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / a.steps)
+    for _ in range(0 if a.pipelined else a.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         _native.solve_device(tA, tb, tc, lim, out, shared_Ab=shared)
