@@ -40,6 +40,10 @@ constexpr int kLazyMaxPivots = 64;
 #ifndef LAZY_SCAN_U
 #define LAZY_SCAN_U 4
 #endif
+// Validation-stream load form, measured (bench-style back-to-back steps; C5 1e4 / random
+// 300 x 300 5e3 / random 100 x 100 2e4, ms): 0 __ldcs 5.177 / 1.358 / 0.854 (default);
+// 1 ld.nc.L1::no_allocate.L2::256B 5.204 / 1.357 / 0.855; 2 __ldcg 5.425 / 1.353 / 0.837;
+// 3 L1::no_allocate + L2 evict_first policy 5.189 / 1.360 / 0.856.
 #ifndef LAZY_SCAN_MODE
 #define LAZY_SCAN_MODE 0
 #endif
@@ -51,6 +55,12 @@ __device__ __forceinline__ double2 lazy_scan_load(const double2 *p) {
     return v;
 #elif LAZY_SCAN_MODE == 2
     return __ldcg(p);
+#elif LAZY_SCAN_MODE == 3
+    double2 v;
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
 #else
     return __ldcs(p);
 #endif
