@@ -100,20 +100,31 @@ __device__ __forceinline__ void sts_v2_f64(unsigned addr, double x, double y) {
 // Rank-1 update of this row's tile slots, col pairs p: t -= fs * r, software-pipelined by hand
 // (the tile and rvec share the shared-memory array, so the compiler would serialise each
 // load behind the previous store): pair p+1 and its pivot-row entries load before pair p stores.
+// CM_TILE_DEPTH: column pairs loaded ahead of the one being updated.  The tile loop's stalls
+// are mostly shared-memory results (C3 source page: 50-64% short_sb), but deeper prefetch
+// measured no better (bench-style steps, ms, depth 1 / 2 / 3): C3 2e4 71.9, 71.5 / 71.8,
+// 71.3 / 71.3, 71.4; C4 1e6 37.19 / 38.14 / 38.20; afiro 150 x 150 (cm8) 57.9 / 59.6 / 60.6.
+#ifndef CM_TILE_DEPTH
+#define CM_TILE_DEPTH 1
+#endif
 template <int R, int S, int ST>
 __device__ __forceinline__ void cm_update_tile(double *tile, int row, const double *rvec, double fs) {
-    constexpr int NP = S / 2;
+    constexpr int NP = S / 2, DP = CM_TILE_DEPTH, NB = DP + 1;
     const unsigned ta = (unsigned)__cvta_generic_to_shared(tile) + 16u * row;
     const unsigned ra = (unsigned)__cvta_generic_to_shared(rvec + R);
-    double t[2][2], r[2][2];
-    lds_v2_f64(ta, t[0][0], t[0][1]);
-    lds_v2_f64(ra, r[0][0], r[0][1]);
+    double t[NB][2], r[NB][2];
+#pragma unroll
+    for (int p = 0; p < DP && p < NP; ++p) {
+        lds_v2_f64(ta + 16u * ST * p, t[p][0], t[p][1]);
+        lds_v2_f64(ra + 16u * p, r[p][0], r[p][1]);
+    }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const int b = p & 1;
-        if (p + 1 < NP) {
-            lds_v2_f64(ta + 16u * ST * (p + 1), t[b ^ 1][0], t[b ^ 1][1]);
-            lds_v2_f64(ra + 16u * (p + 1), r[b ^ 1][0], r[b ^ 1][1]);
+        const int b = p % NB;
+        if (p + DP < NP) {
+            const int bn = (p + DP) % NB;
+            lds_v2_f64(ta + 16u * ST * (p + DP), t[bn][0], t[bn][1]);
+            lds_v2_f64(ra + 16u * (p + DP), r[bn][0], r[bn][1]);
         }
         sts_v2_f64(ta + 16u * ST * p, __dsub_rn(t[b][0], __dmul_rn(fs, r[b][0])),
                    __dsub_rn(t[b][1], __dmul_rn(fs, r[b][1])));
