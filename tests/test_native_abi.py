@@ -47,6 +47,19 @@ def test_kernel_variant_selection(m, n, family):
     assert _native.kernel_variant(m, n).startswith(family)
 
 
+@pytest.mark.parametrize("m,n,family", [(64, 8, "ctab_r2_s8"), (128, 8, "ctab_r4_s8"), (64, 16, "ctab_r2_s16"),
+                                        (40, 16, "lazy+cm2_r16_s16"), (100, 16, "lazy+cm4_r32_s0"),
+                                        (200, 8, "lazy+cm8")])
+def test_narrow_lps_dispatch(m, n, family, monkeypatch):
+    """Narrow LPs (n <= 8, or n <= 16 at 49..64 rows) go to the one-warp condensed kernel
+    (measured faster than the multi-warp form plus its lazy pre-pass); BLP_CMULTI=3 forces
+    the multi-warp form for every 33..128-row shape; beyond 128 rows there is no one-warp form."""
+    assert _native.kernel_variant(m, n) == family or _native.kernel_variant(m, n).startswith(family)
+    monkeypatch.setenv("BLP_CMULTI", "3")
+    v = _native.kernel_variant(m, n)
+    assert v.startswith("lazy+cm"), v
+
+
 def test_kernel_variant_support_mode():
     """Support mode (one A, b): the condensed kernels run without the lazy pass ahead of
     them (their shared phase 1 applies instead)."""
